@@ -1,0 +1,366 @@
+// hmm_capi.cu — the extern "C" boundary (include/loghmm_b200.h).
+//
+// Host-side argument checking, launch geometry, shared-memory carve and
+// dtype / K / family dispatch.  No allocation, no global mutable state.
+#include <algorithm>
+#include <cstring>
+
+#include "hmm_large.cuh"
+#include "hmm_launch.cuh"
+#include "hmm_mstep.cuh"
+
+namespace lhmm {
+#define X(K) LHMM_EXTERN_INST(float, K) LHMM_EXTERN_INST(double, K)
+X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
+#undef X
+
+// ---- standalone emission kernel (emission_log_matrix) --------------------
+template <typename R>
+__global__ void __launch_bounds__(256) emission_kernel(const loghmm_model_t* __restrict__ m,
+                                                       const R* __restrict__ y0,
+                                                       const R* __restrict__ y1, int64_t N,
+                                                       int K, const double* lut, int lut_n,
+                                                       R* __restrict__ out) {
+  const bool two = m->n_streams > 1;
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    bool oob = false;
+    const R v0 = y0[n];
+    const R v1 = two ? y1[n] : R(0);
+    for (int j = 0; j < K; ++j) {
+      R v = exact_logb<R>(m->em[0][j], v0, lut, lut_n, oob);
+      if (two) v = Num<R>::add(v, exact_logb<R>(m->em[1][j], v1, lut, lut_n, oob));
+      out[n * K + j] = v;
+    }
+  }
+}
+
+static inline int cfg_of(const loghmm_model_t* h, int* fams_mask) {
+  const int K = h->K;
+  int m0 = 0, m1 = 0;
+  for (int j = 0; j < K; ++j) {
+    m0 |= 1 << h->em[0][j].family;
+    if (h->n_streams > 1) m1 |= 1 << h->em[1][j].family;
+  }
+  *fams_mask = (m0 & 0xffff) | ((m1 & 0xffff) << 16);
+  if (h->n_streams == 1) {
+    if (m0 == (1 << LOGHMM_FAM_GAUSSIAN)) return kCfgGauss;
+    if (m0 == (1 << LOGHMM_FAM_STUDENT_T)) return kCfgStudent;
+    if (m0 == (1 << LOGHMM_FAM_GAMMA)) return kCfgGamma;
+    if (m0 == (1 << LOGHMM_FAM_VON_MISES)) return kCfgVonMises;
+    if (m0 == (1 << LOGHMM_FAM_POISSON)) return kCfgPoisson;
+  } else if (m0 == (1 << LOGHMM_FAM_GAMMA) && m1 == (1 << LOGHMM_FAM_VON_MISES)) {
+    return kCfgGammaVM;
+  }
+  return kCfgMixed;
+}
+
+static inline int gcd_(int a, int b) { return b ? gcd_(b, a % b) : a; }
+
+// Launch geometry for the K<=8 forward-backward kernel.
+struct FBGeom {
+  bool global;
+  int L_align, Lmax, y_pitch, a_pitch, s_pitch, warp_elems, wpb;
+  size_t smem;
+};
+
+static FBGeom fb_geom(int K, int esz, int n_streams, int64_t max_T) {
+  FBGeom g{};
+  const int kb = K * esz;
+  g.L_align = 16 / gcd_(16, kb);
+  int L = (int)((max_T + kWarp - 1) / kWarp);
+  if (L < 1) L = 1;
+  g.Lmax = ((L + g.L_align - 1) / g.L_align) * g.L_align;
+  g.y_pitch = g.Lmax | 1;  // odd pitch: lane rows fall in distinct banks
+  const int V = (kb % 16 == 0) ? 16 : (kb % 8 == 0) ? 8 : 4;
+  int aunits = g.Lmax * kb / V;
+  if ((aunits & 1) == 0) aunits += 1;
+  g.a_pitch = aunits * V / esz;
+  int sunits = kSlab * kb / 16;
+  if ((sunits & 1) == 0) sunits += 1;
+  g.s_pitch = sunits * 16 / esz;
+  const int64_t smem_elems = (int64_t)kWarp * (g.y_pitch * n_streams + g.a_pitch + 2 * g.s_pitch);
+  const int64_t bytes = smem_elems * esz;
+  g.global = bytes > 110 * 1024;
+  g.warp_elems = g.global ? kWarp * 2 * g.s_pitch : (int)smem_elems;
+  const int64_t wbytes = (int64_t)g.warp_elems * esz;
+  g.wpb = (int)std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / wbytes));
+  g.smem = (size_t)(wbytes * g.wpb);
+  return g;
+}
+
+struct VitGeom {
+  bool global;
+  int wpb;
+  int64_t plane_words;
+  int warp_words;
+  size_t smem;
+};
+
+static VitGeom vit_geom(int K, int64_t max_T) {
+  VitGeom g{};
+  const int NP = K <= 1 ? 0 : K <= 2 ? 1 : K <= 4 ? 2 : 3;
+  g.plane_words = ((max_T + 31) / 32) * 32 * std::max(NP, 1);
+  const int64_t stage_words = 2 * kWarp * kPathPitch;
+  g.global = g.plane_words > 12 * 1024;  // > 48 KB of planes per warp
+  g.warp_words = (int)(stage_words + (g.global ? 0 : g.plane_words));
+  g.warp_words = (g.warp_words + 3) & ~3;
+  g.wpb = 4;
+  g.smem = (size_t)g.warp_words * 4 * g.wpb;
+  return g;
+}
+
+template <typename R>
+static cudaError_t dispatch_fb_small(int K, const FBArgs& a, int cfg, bool gl, dim3 grid,
+                                     dim3 block, size_t smem, cudaStream_t st) {
+  switch (K) {
+    case 1: return launch_fb_small<R, 1>(a, cfg, gl, grid, block, smem, st);
+    case 2: return launch_fb_small<R, 2>(a, cfg, gl, grid, block, smem, st);
+    case 3: return launch_fb_small<R, 3>(a, cfg, gl, grid, block, smem, st);
+    case 4: return launch_fb_small<R, 4>(a, cfg, gl, grid, block, smem, st);
+    case 5: return launch_fb_small<R, 5>(a, cfg, gl, grid, block, smem, st);
+    case 6: return launch_fb_small<R, 6>(a, cfg, gl, grid, block, smem, st);
+    case 7: return launch_fb_small<R, 7>(a, cfg, gl, grid, block, smem, st);
+    default: return launch_fb_small<R, 8>(a, cfg, gl, grid, block, smem, st);
+  }
+}
+
+template <typename R>
+static cudaError_t dispatch_vit_small(int K, const VitArgs& a, bool gl, dim3 grid, dim3 block,
+                                      size_t smem, cudaStream_t st) {
+  switch (K) {
+    case 1: return launch_vit_small<R, 1>(a, gl, grid, block, smem, st);
+    case 2: return launch_vit_small<R, 2>(a, gl, grid, block, smem, st);
+    case 3: return launch_vit_small<R, 3>(a, gl, grid, block, smem, st);
+    case 4: return launch_vit_small<R, 4>(a, gl, grid, block, smem, st);
+    case 5: return launch_vit_small<R, 5>(a, gl, grid, block, smem, st);
+    case 6: return launch_vit_small<R, 6>(a, gl, grid, block, smem, st);
+    case 7: return launch_vit_small<R, 7>(a, gl, grid, block, smem, st);
+    default: return launch_vit_small<R, 8>(a, gl, grid, block, smem, st);
+  }
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace lhmm
+
+using namespace lhmm;
+
+extern "C" {
+
+int32_t loghmm_abi_version(void) { return LOGHMM_ABI_VERSION; }
+
+size_t loghmm_model_bytes(void) { return sizeof(loghmm_model_t); }
+
+int64_t loghmm_stats_width(int32_t K, int32_t n_streams) {
+  (void)n_streams;
+  return (int64_t)K * K + 2 * (int64_t)K + 2 * (int64_t)K * LOGHMM_NSLOT;
+}
+
+size_t loghmm_fb_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N, int64_t max_T) {
+  (void)B;
+  const int esz = dtype == LOGHMM_F64 ? 8 : 4;
+  if (K > 8) return align256((size_t)N * K * esz);
+  FBGeom g = fb_geom(K, esz, 2, max_T);
+  return g.global ? align256((size_t)N * K * esz) : 0;
+}
+
+size_t loghmm_viterbi_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N,
+                                      int64_t max_T) {
+  (void)dtype;
+  if (K > 8) return align256((size_t)N * K);
+  VitGeom g = vit_geom(K, max_T);
+  if (!g.global) return 0;
+  const int64_t G = kWarp / K;
+  const int64_t warps = (B + G - 1) / G;
+  return align256((size_t)warps * g.plane_words * 4);
+}
+
+int32_t loghmm_emission(int32_t dtype, const loghmm_model_t* h_desc, const loghmm_model_t* model,
+                        const void* y0, const void* y1, int64_t N, const double* lgamma_lut,
+                        int32_t lut_n, void* log_b, void* stream) {
+  if (!h_desc || !model || !y0 || !log_b || N < 0) return LOGHMM_EINVAL;
+  const int K = h_desc->K;
+  if (K < 1 || K > LOGHMM_MAX_STATES) return LOGHMM_EINVAL;
+  if (h_desc->n_streams > 1 && !y1) return LOGHMM_EINVAL;
+  if (N == 0) return LOGHMM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t blocks = std::min<int64_t>((N + 255) / 256, 148 * 16);
+  if (dtype == LOGHMM_F64)
+    emission_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(model, (const double*)y0,
+                                                              (const double*)y1, N, K, lgamma_lut,
+                                                              lut_n, (double*)log_b);
+  else
+    emission_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(model, (const float*)y0,
+                                                             (const float*)y1, N, K, lgamma_lut,
+                                                             lut_n, (float*)log_b);
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
+                                const loghmm_model_t* model, const void* y0, const void* y1,
+                                const int64_t* offsets, int64_t B, int64_t N, int64_t max_T,
+                                const double* lgamma_lut, int32_t lut_n, void* log_alpha,
+                                void* log_beta, void* gamma, void* xi, double* ll,
+                                double* partials, int64_t* flags, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (!h_desc || !model || !y0 || !offsets || !ll || B < 0 || N < 0) return LOGHMM_EINVAL;
+  const int K = h_desc->K;
+  if (K < 1 || K > LOGHMM_MAX_STATES) return LOGHMM_EINVAL;
+  if (h_desc->n_streams > 1 && !y1) return LOGHMM_EINVAL;
+  if (B == 0) return LOGHMM_OK;
+  const int esz = dtype == LOGHMM_F64 ? 8 : 4;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (workspace_bytes < loghmm_fb_workspace_bytes(dtype, K, B, N, max_T)) return LOGHMM_EWORKSPACE;
+  FBArgs a{};
+  a.model = model;
+  a.y0 = y0;
+  a.y1 = h_desc->n_streams > 1 ? y1 : nullptr;
+  a.offsets = offsets;
+  a.B = B;
+  a.lut = lgamma_lut;
+  a.lut_n = lut_n;
+  a.n_streams = h_desc->n_streams;
+  a.log_alpha = log_alpha;
+  a.log_beta = log_beta;
+  a.gamma = gamma;
+  a.xi = xi;
+  a.ll = ll;
+  a.partials = partials;
+  a.flags = flags;
+  a.alpha_ws = workspace;
+  a.stats_width = loghmm_stats_width(K, h_desc->n_streams);
+  int fams = 0;
+  const int cfg = cfg_of(h_desc, &fams);
+  a.stream_fams = fams;
+  cudaError_t e;
+  if (K <= 8) {
+    FBGeom g = fb_geom(K, esz, h_desc->n_streams, max_T);
+    a.L_align = g.L_align;
+    a.Lmax = g.Lmax;
+    a.y_pitch = g.y_pitch;
+    a.a_pitch = g.a_pitch;
+    a.s_pitch = g.s_pitch;
+    a.warp_smem_elems = g.warp_elems;
+    dim3 grid((unsigned)((B + g.wpb - 1) / g.wpb)), block(32 * g.wpb);
+    e = dtype == LOGHMM_F64 ? dispatch_fb_small<double>(K, a, cfg, g.global, grid, block, g.smem, st)
+                            : dispatch_fb_small<float>(K, a, cfg, g.global, grid, block, g.smem, st);
+  } else {
+    const int threads = 32 * ((K + 31) / 32);
+    const size_t smem = (size_t)(2 * K * K + K + 32) * esz;
+    if (dtype == LOGHMM_F64) {
+      cudaFuncSetAttribute(fb_large_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      fb_large_kernel<double><<<(unsigned)B, threads, smem, st>>>(a, K);
+    } else {
+      cudaFuncSetAttribute(fb_large_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      fb_large_kernel<float><<<(unsigned)B, threads, smem, st>>>(a, K);
+    }
+    e = cudaGetLastError();
+  }
+  return e == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm_model_t* model,
+                       const void* y0, const void* y1, const int64_t* offsets, int64_t B,
+                       int64_t N, int64_t max_T, const double* lgamma_lut, int32_t lut_n,
+                       int64_t* path, double* log_joint, uint8_t* back, int64_t* flags,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (!h_desc || !model || !y0 || !offsets || !path || !log_joint || B < 0) return LOGHMM_EINVAL;
+  const int K = h_desc->K;
+  if (K < 1 || K > LOGHMM_MAX_STATES) return LOGHMM_EINVAL;
+  if (h_desc->n_streams > 1 && !y1) return LOGHMM_EINVAL;
+  if (B == 0) return LOGHMM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (workspace_bytes < loghmm_viterbi_workspace_bytes(dtype, K, B, N, max_T))
+    return LOGHMM_EWORKSPACE;
+  VitArgs a{};
+  a.model = model;
+  a.y0 = y0;
+  a.y1 = h_desc->n_streams > 1 ? y1 : nullptr;
+  a.offsets = offsets;
+  a.B = B;
+  a.lut = lgamma_lut;
+  a.lut_n = lut_n;
+  a.n_streams = h_desc->n_streams;
+  a.path = path;
+  a.log_joint = log_joint;
+  a.back = back;
+  a.flags = flags;
+  cudaError_t e;
+  if (K <= 8) {
+    VitGeom g = vit_geom(K, max_T);
+    a.planes_ws = (uint32_t*)workspace;
+    a.plane_words = g.plane_words;
+    a.warp_smem_words = g.warp_words;
+    const int64_t G = kWarp / K;
+    const int64_t warps = (B + G - 1) / G;
+    dim3 grid((unsigned)((warps + g.wpb - 1) / g.wpb)), block(32 * g.wpb);
+    e = dtype == LOGHMM_F64 ? dispatch_vit_small<double>(K, a, g.global, grid, block, g.smem, st)
+                            : dispatch_vit_small<float>(K, a, g.global, grid, block, g.smem, st);
+  } else {
+    const int esz = dtype == LOGHMM_F64 ? 8 : 4;
+    const int threads = 32 * ((K + 31) / 32);
+    const size_t smem = (size_t)(K * K + K) * esz + 256 * (size_t)K;
+    if (dtype == LOGHMM_F64) {
+      cudaFuncSetAttribute(viterbi_large_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      viterbi_large_kernel<double><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace);
+    } else {
+      cudaFuncSetAttribute(viterbi_large_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      viterbi_large_kernel<float><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace);
+    }
+    e = cudaGetLastError();
+  }
+  return e == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+int32_t loghmm_reduce_stats(const double* partials, const double* ll, int64_t B, int64_t width,
+                            double* totals, void* stream) {
+  if (!partials || !ll || !totals || B < 0 || width < 0) return LOGHMM_EINVAL;
+  reduce_stats_kernel<<<(unsigned)(width + 1), 256, 0, (cudaStream_t)stream>>>(partials, ll, B,
+                                                                                 width, totals);
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64_t n_sequences,
+                     double collapse_epsilon, double nu_ceiling, double nu_tol, int32_t max_newton,
+                     loghmm_model_t* model_out, int32_t* status, double* guard_state,
+                     void* stream) {
+  if (!model_in || !totals || !model_out || !status || !guard_state || n_sequences < 1)
+    return LOGHMM_EINVAL;
+  mstep_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(model_in, totals, n_sequences,
+                                                    collapse_epsilon, nu_ceiling, nu_tol,
+                                                    max_newton, model_out, status, guard_state);
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+size_t loghmm_guard_workspace_bytes(int32_t K, int64_t N) {
+  (void)N;
+  return align256((size_t)148 * 4 * K * LOGHMM_GUARD_CANDIDATES * sizeof(double) + 16);
+}
+
+int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const void* y0,
+                             const void* gamma, int64_t N, int32_t K, int32_t stream_index,
+                             int32_t n_candidates, double* guard_state, int32_t* status,
+                             int32_t* need_more, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  if (!model_out || !y0 || !gamma || !guard_state || !status || !need_more || K < 1 ||
+      n_candidates < 2 || n_candidates > LOGHMM_GUARD_CANDIDATES)
+    return LOGHMM_EINVAL;
+  if (workspace_bytes < loghmm_guard_workspace_bytes(K, N)) return LOGHMM_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nblocks = 148 * 4;
+  double* part = (double*)workspace;
+  if (dtype == LOGHMM_F64)
+    student_guard_kernel<double><<<nblocks, 256, 0, st>>>((const double*)y0, (const double*)gamma,
+                                                          N, K, stream_index, guard_state,
+                                                          n_candidates, part);
+  else
+    student_guard_kernel<float><<<nblocks, 256, 0, st>>>((const float*)y0, (const float*)gamma, N,
+                                                         K, stream_index, guard_state,
+                                                         n_candidates, part);
+  guard_select_kernel<<<1, 64, 0, st>>>(model_out, K, stream_index, guard_state, n_candidates,
+                                        part, nblocks, status, need_more);
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+}  // extern "C"

@@ -1,0 +1,904 @@
+// hmm_fb.cuh — fused batched forward-backward + E-step statistics, K <= 8.
+//
+// One warp owns one sequence.  The sequence is cut into 32 contiguous chunks,
+// one per lane, and the serial log-space recursions of the reference
+//   inference.py:129-137 (_forward_from_log_b)
+//   inference.py:140-146 (_backward_from_log_b)
+// are evaluated as an associative scan over chunk transfer operators:
+//
+//  phase 1  each lane builds M_c = prod_{t in chunk} A diag(b_t) in linear
+//           space (power-of-two normalised, log offset kept in fp64).  The
+//           same operator serves both directions: alpha_end = alpha_start M_c
+//           and beta_start = M_c beta_end.
+//  phase 2  Hillis-Steele scans over the 32 lanes (warp shuffles) give every
+//           lane its entering forward vector and exiting backward vector, and
+//           the sequence log-likelihood.
+//  phase 3  each lane re-runs its chunk: forward writes log_alpha and keeps
+//           the max-normalised alpha in shared memory; backward writes
+//           log_beta and gamma and accumulates xi totals, gamma totals and
+//           the family sufficient statistics (training.py:199-210,221-222).
+//
+// Outputs are staged per lane in shared memory and written as contiguous
+// rows, so every global store instruction is coalesced.  Per-step carried
+// state is (linear vector with max 1, fp64 log offset): this keeps relative
+// precision in fp32 where carrying raw log values of magnitude ~1e3 would not
+// (SURVEY.md §7.3-2).
+#pragma once
+
+#include "hmm_common.cuh"
+
+namespace lhmm {
+
+constexpr int kSlab = 4;  // output staging depth (steps per lane per flush)
+
+struct FBArgs {
+  const loghmm_model_t* model;
+  const void* y0;
+  const void* y1;
+  const int64_t* offsets;
+  int64_t B;
+  const double* lut;
+  int lut_n;
+  int n_streams;
+  void* log_alpha;
+  void* log_beta;
+  void* gamma;
+  void* xi;
+  double* ll;
+  double* partials;
+  int64_t* flags;
+  void* alpha_ws;  // global alpha store [N, K] when kGlobal
+  int64_t stats_width;
+  int L_align;
+  int Lmax;
+  int stream_fams;  // bitmask of families present (for kCfgMixed)
+  // shared-memory carve (elements of R, per warp)
+  int y_pitch;
+  int a_pitch;
+  int s_pitch;
+  int warp_smem_elems;
+};
+
+template <typename R, int K>
+struct VecIO {
+  // Vector width (elements) for a K-vector of R in shared memory.
+  static constexpr int BYTES = K * (int)sizeof(R);
+  static constexpr int VE = (BYTES % 16 == 0) ? 16 / (int)sizeof(R)
+                            : (BYTES % 8 == 0) ? 8 / (int)sizeof(R)
+                                               : 1;
+  static __device__ __forceinline__ void st(R* p, const R (&v)[K]) {
+    if constexpr (sizeof(R) == 4 && VE == 4) {
+#pragma unroll
+      for (int i = 0; i < K; i += 4)
+        *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else if constexpr (sizeof(R) == 4 && VE == 2) {
+#pragma unroll
+      for (int i = 0; i < K; i += 2) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
+    } else if constexpr (sizeof(R) == 8 && VE == 2) {
+#pragma unroll
+      for (int i = 0; i < K; i += 2)
+        *reinterpret_cast<double2*>(p + i) = make_double2((double)v[i], (double)v[i + 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < K; ++i) p[i] = v[i];
+    }
+  }
+  static __device__ __forceinline__ void ld(const R* p, R (&v)[K]) {
+    if constexpr (sizeof(R) == 4 && VE == 4) {
+#pragma unroll
+      for (int i = 0; i < K; i += 4) {
+        float4 q = *reinterpret_cast<const float4*>(p + i);
+        v[i] = q.x; v[i + 1] = q.y; v[i + 2] = q.z; v[i + 3] = q.w;
+      }
+    } else if constexpr (sizeof(R) == 4 && VE == 2) {
+#pragma unroll
+      for (int i = 0; i < K; i += 2) {
+        float2 q = *reinterpret_cast<const float2*>(p + i);
+        v[i] = q.x; v[i + 1] = q.y;
+      }
+    } else if constexpr (sizeof(R) == 8 && VE == 2) {
+#pragma unroll
+      for (int i = 0; i < K; i += 2) {
+        double2 q = *reinterpret_cast<const double2*>(p + i);
+        v[i] = (R)q.x; v[i + 1] = (R)q.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < K; ++i) v[i] = p[i];
+    }
+  }
+};
+
+// Write the staged rows of a slab window to global memory.  Row c (lane c's
+// chunk) covers global steps t0_c + sb + [0, n_c); its bytes are contiguous
+// in the [N, K] output, so lanes cooperatively copy 16-byte units row by row.
+template <typename R, int K>
+__device__ __forceinline__ void flush_slab(R* __restrict__ out, const R* __restrict__ stage,
+                                           int s_pitch, int64_t start, int L, int T, int sb,
+                                           int lane, bool vec_ok) {
+  constexpr int ROW = kSlab * K;  // elements per full row
+  if (vec_ok) {
+    constexpr int EPV = 16 / (int)sizeof(R);
+    constexpr int VPR = (ROW + EPV - 1) / EPV;  // vectors per row (ROW*sizeof(R) % 16 == 0)
+#pragma unroll 1
+    for (int v = lane; v < kWarp * VPR; v += kWarp) {
+      const int c = v / VPR, vi = v % VPR;
+      const int t0 = c * L + sb;
+      int n = T - t0;
+      n = n < 0 ? 0 : (n > kSlab ? kSlab : n);
+      const int ccap = (c + 1) * L - t0;  // steps left in this chunk from sb
+      if (n > ccap) n = ccap;
+      const int nel = n * K;
+      const int e0 = vi * EPV;
+      if (e0 >= nel) continue;
+      R* dst = out + (start + t0) * K + e0;
+      const R* src = stage + c * s_pitch + e0;
+      if (e0 + EPV <= nel) {
+        *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
+      } else {
+        for (int e = 0; e < nel - e0; ++e) dst[e] = src[e];
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int v = lane; v < kWarp * ROW; v += kWarp) {
+      const int c = v / ROW, e = v % ROW;
+      const int t0 = c * L + sb;
+      int n = T - t0;
+      n = n < 0 ? 0 : (n > kSlab ? kSlab : n);
+      const int ccap = (c + 1) * L - t0;
+      if (n > ccap) n = ccap;
+      if (e < n * K) out[(start + t0) * K + e] = stage[c * s_pitch + e];
+    }
+  }
+}
+
+// Matrix product Z = X * Y (K x K), FMA.
+template <typename R, int K>
+__device__ __forceinline__ void matmul(const R (&X)[K][K], const R (&Y)[K][K], R (&Z)[K][K]) {
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      R acc = X[r][0] * Y[0][c];
+#pragma unroll
+      for (int i = 1; i < K; ++i) acc = fma(X[r][i], Y[i][c], acc);
+      Z[r][c] = acc;
+    }
+}
+
+template <typename R, int K>
+__device__ __forceinline__ void normalise_mat(R (&Z)[K][K], double& off) {
+  R m = Z[0][0];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int c = 0; c < K; ++c) m = rmax(m, Z[r][c]);
+  if (m > R(0)) {
+    R s = Num<R>::pow2_normaliser(m, off);
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+#pragma unroll
+      for (int c = 0; c < K; ++c) Z[r][c] *= s;
+  } else {
+    off = -CUDART_INF;
+  }
+}
+
+template <typename R, int K>
+__device__ __forceinline__ void normalise_vec(R (&v)[K], double& off) {
+  R m = v[0];
+#pragma unroll
+  for (int i = 1; i < K; ++i) m = rmax(m, v[i]);
+  if (m > R(0)) {
+    R s = Num<R>::pow2_normaliser(m, off);
+#pragma unroll
+    for (int i = 0; i < K; ++i) v[i] *= s;
+  } else {
+    off = -CUDART_INF;
+  }
+}
+
+template <typename R, int K>
+__device__ __forceinline__ void shfl_mat(R (&Z)[K][K], double& off, const R (&X)[K][K], double xo,
+                                         int delta, bool up) {
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int c = 0; c < K; ++c)
+      Z[r][c] = up ? __shfl_up_sync(kFull, X[r][c], delta) : __shfl_down_sync(kFull, X[r][c], delta);
+  off = up ? __shfl_up_sync(kFull, xo, delta) : __shfl_down_sync(kFull, xo, delta);
+}
+
+// ---------------------------------------------------------------------------
+// Emission evaluation for all states at one step (fast contract).
+// ---------------------------------------------------------------------------
+template <typename R, int K, int CFG>
+struct Emit {
+  EmP<R> e0[K];
+  EmP<R> e1[K];
+  int stream_fams;
+  const double* lut;
+  int lut_n;
+
+  __device__ __forceinline__ void load(const loghmm_model_t* m, int n_streams, int fams,
+                                       const double* lut_, int lut_n_) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      e0[j] = load_emission<R>(m->em[0][j]);
+      if (CFG == kCfgGammaVM || (CFG == kCfgMixed && n_streams > 1))
+        e1[j] = load_emission<R>(m->em[1][j]);
+      else
+        e1[j].fam = LOGHMM_FAM_NONE;
+    }
+    stream_fams = fams;
+    lut = lut_;
+    lut_n = lut_n_;
+  }
+
+  // logb[j] for observation(s) y0 (and y1); also fills the features used by
+  // the statistics.
+  __device__ __forceinline__ void eval(R y0, R y1, ObsFeat<R>& f0, ObsFeat<R>& f1, R (&lb)[K],
+                                       bool& oob) const {
+    if (CFG == kCfgGammaVM) {
+      obs_features<R, kCfgGamma>(f0, y0, lut, lut_n, oob, 0);
+      obs_features<R, kCfgVonMises>(f1, y1, lut, lut_n, oob, 0);
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        lb[j] = fast_logb_fam<R, LOGHMM_FAM_GAMMA>(e0[j], f0) +
+                fast_logb_fam<R, LOGHMM_FAM_VON_MISES>(e1[j], f1);
+    } else if (CFG == kCfgMixed) {
+      obs_features<R, kCfgMixed>(f0, y0, lut, lut_n, oob, stream_fams & 0xffff);
+      obs_features<R, kCfgMixed>(f1, y1, lut, lut_n, oob, stream_fams >> 16);
+#pragma unroll
+      for (int j = 0; j < K; ++j) lb[j] = fast_logb_rt<R>(e0[j], f0) + fast_logb_rt<R>(e1[j], f1);
+    } else {
+      obs_features<R, CFG>(f0, y0, lut, lut_n, oob, 0);
+#pragma unroll
+      for (int j = 0; j < K; ++j) lb[j] = fast_logb_fam<R, CFG>(e0[j], f0);
+    }
+  }
+};
+
+// Family sufficient statistics of one state at one step (slots in acc[6]).
+//  gaussian : w, w*d, w*d^2                 d = y - mu_current   (fit_gaussian :632)
+//  poisson  : w, w*y, [w>0 & invalid]                             (fit_poisson :658)
+//  gamma    : w, w*d, w*d^2, w*log y, [w>0 & y<=0]  d = y - mean  (fit_gamma_nr :764)
+//  von_mises: w, w*sin y, w*cos y, [w>0 & !finite]                (fit_vonmises :874)
+//  student_t: w, w*u, w*u*d, w*u*d^2, w*(log u - u)  at current params,
+//             u = (nu+1)/(nu+z^2), d = y - mu                     (ECME pass A :1043-1054)
+template <typename R, int FAM>
+__device__ __forceinline__ void stat_acc(R (&acc)[LOGHMM_NSLOT], R w, const EmP<R>& p,
+                                         const ObsFeat<R>& f) {
+  const bool pos = w > R(0);
+  if (FAM == LOGHMM_FAM_GAUSSIAN) {
+    R d = f.y - p.q[0];
+    R wd = w * d;
+    acc[0] += w;
+    acc[1] += wd;
+    acc[2] = fma(wd, d, acc[2]);
+  } else if (FAM == LOGHMM_FAM_POISSON) {
+    acc[0] += w;
+    if (f.pois_ok) acc[1] = fma(w, f.y, acc[1]);
+    else if (pos) acc[2] += R(1);
+  } else if (FAM == LOGHMM_FAM_GAMMA) {
+    acc[0] += w;
+    if (f.y > R(0)) {
+      R d = f.y - p.q[3];
+      R wd = w * d;
+      acc[1] += wd;
+      acc[2] = fma(wd, d, acc[2]);
+      acc[3] = fma(w, f.logy, acc[3]);
+    } else if (pos) {
+      acc[4] += R(1);
+    }
+  } else if (FAM == LOGHMM_FAM_VON_MISES) {
+    acc[0] += w;
+    if (isfinite(f.y)) {
+      acc[1] = fma(w, f.siny, acc[1]);
+      acc[2] = fma(w, f.cosy, acc[2]);
+    } else if (pos) {
+      acc[3] += R(1);
+    }
+  } else if (FAM == LOGHMM_FAM_STUDENT_T) {
+    R d = f.y - p.q[0];
+    R z = d * p.q[1];
+    R u = (p.q[5] + R(1)) / (p.q[5] + z * z);
+    R wu = w * u;
+    acc[0] += w;
+    acc[1] += wu;
+    acc[2] = fma(wu, d, acc[2]);
+    acc[3] = fma(wu * d, d, acc[3]);
+    if (pos) acc[4] = fma(w, Num<R>::alog(u) - u, acc[4]);
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ void stat_acc_rt(R (&acc)[LOGHMM_NSLOT], R w, const EmP<R>& p,
+                                            const ObsFeat<R>& f) {
+  switch (p.fam) {
+    case LOGHMM_FAM_GAUSSIAN: stat_acc<R, LOGHMM_FAM_GAUSSIAN>(acc, w, p, f); break;
+    case LOGHMM_FAM_STUDENT_T: stat_acc<R, LOGHMM_FAM_STUDENT_T>(acc, w, p, f); break;
+    case LOGHMM_FAM_GAMMA: stat_acc<R, LOGHMM_FAM_GAMMA>(acc, w, p, f); break;
+    case LOGHMM_FAM_VON_MISES: stat_acc<R, LOGHMM_FAM_VON_MISES>(acc, w, p, f); break;
+    case LOGHMM_FAM_POISSON: stat_acc<R, LOGHMM_FAM_POISSON>(acc, w, p, f); break;
+    default: break;
+  }
+}
+
+template <int CFG>
+struct CfgTraits {
+  static constexpr int S = (CFG == kCfgGammaVM || CFG == kCfgMixed) ? 2 : 1;  // stat streams
+  static constexpr int F0 = CFG == kCfgGauss     ? LOGHMM_FAM_GAUSSIAN
+                            : CFG == kCfgStudent  ? LOGHMM_FAM_STUDENT_T
+                            : CFG == kCfgGamma    ? LOGHMM_FAM_GAMMA
+                            : CFG == kCfgVonMises ? LOGHMM_FAM_VON_MISES
+                            : CFG == kCfgPoisson  ? LOGHMM_FAM_POISSON
+                            : CFG == kCfgGammaVM  ? LOGHMM_FAM_GAMMA
+                                                  : -1;
+  static constexpr int F1 = CFG == kCfgGammaVM ? LOGHMM_FAM_VON_MISES : -1;
+  static constexpr int NS0 = F0 == LOGHMM_FAM_GAUSSIAN    ? 3
+                             : F0 == LOGHMM_FAM_POISSON   ? 3
+                             : F0 == LOGHMM_FAM_GAMMA     ? 5
+                             : F0 == LOGHMM_FAM_VON_MISES ? 4
+                             : F0 == LOGHMM_FAM_STUDENT_T ? 5
+                                                          : LOGHMM_NSLOT;
+  static constexpr int NS1 = F1 == LOGHMM_FAM_VON_MISES ? 4 : LOGHMM_NSLOT;
+};
+
+template <typename R, int K, int CFG>
+__device__ __forceinline__ void stats_step(R (&st)[CfgTraits<CFG>::S][K][LOGHMM_NSLOT],
+                                           const R (&g)[K], const Emit<R, K, CFG>& em,
+                                           const ObsFeat<R>& f0, const ObsFeat<R>& f1) {
+  typedef CfgTraits<CFG> TR;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if constexpr (TR::F0 >= 0) {
+      stat_acc<R, TR::F0>(st[0][j], g[j], em.e0[j], f0);
+    } else {
+      stat_acc_rt<R>(st[0][j], g[j], em.e0[j], f0);
+    }
+    if constexpr (TR::S > 1) {
+      if constexpr (TR::F1 >= 0) {
+        stat_acc<R, TR::F1>(st[1][j], g[j], em.e1[j], f1);
+      } else {
+        stat_acc_rt<R>(st[1][j], g[j], em.e1[j], f1);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.
+// ---------------------------------------------------------------------------
+template <typename R, int K, int CFG, bool kGlobal>
+__global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
+  typedef Num<R> N;
+  typedef CfgTraits<CFG> TR;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (b >= a.B) return;
+
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  int L = (T + kWarp - 1) / kWarp;
+  L = ((L + a.L_align - 1) / a.L_align) * a.L_align;
+  if (L < 1) L = 1;
+  const int t0 = lane * L;
+  const int t1 = min(t0 + L, T);
+  const int len = t1 > t0 ? t1 - t0 : 0;
+
+  const R* __restrict__ y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const R* __restrict__ y1g = a.y1 ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  const bool two = (a.n_streams > 1);
+
+  R* wsm = reinterpret_cast<R*>(smem_raw) + (size_t)wib * a.warp_smem_elems;
+  R* ybuf0 = wsm;
+  R* ybuf1 = ybuf0 + kWarp * a.y_pitch;
+  R* abuf = ybuf1 + (two ? kWarp * a.y_pitch : 0);
+  R* stA = abuf + kWarp * a.a_pitch;
+  R* stB = stA + kWarp * a.s_pitch;
+  if (kGlobal) {
+    stA = wsm;
+    stB = stA + kWarp * a.s_pitch;
+  }
+
+  // ---- model -------------------------------------------------------------
+  const loghmm_model_t* __restrict__ md = a.model;
+  R Am[K][K];
+  R minA = R(1);
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      Am[i][j] = (R)md->A[i * K + j];
+      minA = Am[i][j] < minA ? Am[i][j] : minA;
+    }
+  R lpi[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) lpi[j] = (R)md->log_pi[j];
+  Emit<R, K, CFG> em;
+  em.load(md, a.n_streams, a.stream_fams, a.lut, a.lut_n);
+  // Normalise the operator every `nn` steps: the max entry decays by at most
+  // min(A) per step (choose the column of the emission maximum), so nn steps
+  // keep it above 2^-100 (fp32) / 2^-900 (fp64).
+  int nn = 1;
+  if (minA > R(0)) {
+    const double lg = -log2((double)minA);
+    const double budget = sizeof(R) == 4 ? 100.0 : 900.0;
+    nn = lg <= 0.0 ? 8 : (int)fmin(8.0, fmax(1.0, floor(budget / lg)));
+  }
+
+  // ---- stage y into shared memory (coalesced), chunk-major with odd pitch --
+  if (!kGlobal) {
+#pragma unroll 1
+    for (int c = 0; c < kWarp; ++c) {
+      const int base = c * L;
+#pragma unroll 1
+      for (int s = lane; s < L; s += kWarp) {
+        const int t = base + s;
+        if (t < T) {
+          ybuf0[c * a.y_pitch + s] = y0g[t];
+          if (two) ybuf1[c * a.y_pitch + s] = y1g[t];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  auto yat0 = [&](int s) -> R { return kGlobal ? y0g[t0 + s] : ybuf0[lane * a.y_pitch + s]; };
+  auto yat1 = [&](int s) -> R {
+    return two ? (kGlobal ? y1g[t0 + s] : ybuf1[lane * a.y_pitch + s]) : R(0);
+  };
+
+  bool oob = false;
+  bool nan_seen = false;
+  int dead_t = INT_MAX;
+
+  // ---- phase 1: chunk transfer operator --------------------------------
+  R Mop[K][K];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int c = 0; c < K; ++c) Mop[r][c] = r == c ? R(1) : R(0);
+  double moff = 0.0;
+  R seed_u[K];  // lane 0: log pi + log b_0
+#pragma unroll
+  for (int j = 0; j < K; ++j) seed_u[j] = N::ninf();
+  {
+    int cnt = 0;
+#pragma unroll 1
+    for (int s = 0; s < len; ++s) {
+      const int t = t0 + s;
+      const R yv0 = yat0(s), yv1 = yat1(s);
+      if (isnan(yv0) || isnan(yv1)) nan_seen = true;
+      ObsFeat<R> f0, f1;
+      R lb[K];
+      em.eval(yv0, yv1, f0, f1, lb, oob);
+      R m = lb[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) m = rmax(m, lb[j]);
+      if (!(m > N::ninf())) {
+        if (t < dead_t) dead_t = t;
+      }
+      if (t == 0) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) seed_u[j] = lpi[j] + lb[j];
+        continue;
+      }
+      const bool finite_m = m > N::ninf();
+      R bt[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) bt[j] = finite_m ? N::fexp(lb[j] - m) : R(0);
+      R AD[K][K];
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = 0; j < K; ++j) AD[i][j] = Am[i][j] * bt[j];
+      R Nw[K][K];
+      matmul<R, K>(Mop, AD, Nw);
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) Mop[r][c] = Nw[r][c];
+      moff += finite_m ? (double)m : -CUDART_INF;
+      if (++cnt == nn) {
+        cnt = 0;
+        normalise_mat<R, K>(Mop, moff);
+      }
+    }
+    normalise_mat<R, K>(Mop, moff);
+  }
+
+  // ---- phase 2a: forward scan (inclusive prefix of operators) -------------
+  R a_in[K];
+  double lam_in;
+  double LL;
+  {
+    R Q[K][K];
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+#pragma unroll
+      for (int c = 0; c < K; ++c) Q[r][c] = Mop[r][c];
+    double qo = moff;
+#pragma unroll 1
+    for (int d = 1; d < kWarp; d <<= 1) {
+      R P[K][K];
+      double po;
+      shfl_mat<R, K>(P, po, Q, qo, d, true);
+      if (lane >= d) {
+        R Z[K][K];
+        matmul<R, K>(P, Q, Z);
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+#pragma unroll
+          for (int c = 0; c < K; ++c) Q[r][c] = Z[r][c];
+        qo += po;
+        normalise_mat<R, K>(Q, qo);
+      }
+    }
+    // seed vector alpha_0 (lane 0), broadcast
+    R sm = seed_u[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) sm = rmax(sm, seed_u[j]);
+    R sv[K];
+    const bool sfin = sm > N::ninf();
+#pragma unroll
+    for (int j = 0; j < K; ++j) sv[j] = sfin ? N::fexp(seed_u[j] - sm) : R(0);
+    double so = sfin ? (double)sm : -CUDART_INF;
+#pragma unroll
+    for (int j = 0; j < K; ++j) sv[j] = __shfl_sync(kFull, sv[j], 0);
+    so = __shfl_sync(kFull, so, 0);
+    // v_c = seed * Q_c
+    R v[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      R acc = sv[0] * Q[0][c];
+#pragma unroll
+      for (int i = 1; i < K; ++i) acc = fma(sv[i], Q[i][c], acc);
+      v[c] = acc;
+    }
+    double vo = so + qo;
+    normalise_vec<R, K>(v, vo);
+    // log-likelihood from lane 31
+    R vs = v[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) vs += v[j];
+    double llv = vo + (double)N::flog(vs);
+    if (!(vs > R(0))) llv = -CUDART_INF;
+    LL = __shfl_sync(kFull, llv, kWarp - 1);
+    // entering vector for lane c = v_{c-1}
+#pragma unroll
+    for (int j = 0; j < K; ++j) a_in[j] = __shfl_up_sync(kFull, v[j], 1);
+    lam_in = __shfl_up_sync(kFull, vo, 1);
+    // rescale to max 1 exactly representable (pow2 normalised already)
+  }
+
+  // ---- phase 2b: backward scan (inclusive suffix of operators) ------------
+  R r_ex[K];
+  double rho_ex;
+  {
+    R S[K][K];
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+#pragma unroll
+      for (int c = 0; c < K; ++c) S[r][c] = Mop[r][c];
+    double so = moff;
+#pragma unroll 1
+    for (int d = 1; d < kWarp; d <<= 1) {
+      R Y[K][K];
+      double yo;
+      shfl_mat<R, K>(Y, yo, S, so, d, false);
+      if (lane + d < kWarp) {
+        R Z[K][K];
+        matmul<R, K>(S, Y, Z);
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+#pragma unroll
+          for (int c = 0; c < K; ++c) S[r][c] = Z[r][c];
+        so += yo;
+        normalise_mat<R, K>(S, so);
+      }
+    }
+    R z[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      R acc = S[r][0];
+#pragma unroll
+      for (int c = 1; c < K; ++c) acc += S[r][c];
+      z[r] = acc;
+    }
+    double zo = so;
+    R e[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) e[j] = __shfl_down_sync(kFull, z[j], 1);
+    double eo = __shfl_down_sync(kFull, zo, 1);
+    if (lane == kWarp - 1) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) e[j] = R(1);
+      eo = 0.0;
+    }
+    R me = e[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) me = rmax(me, e[j]);
+    if (me > R(0)) {
+      const R lme = N::flog(me);
+#pragma unroll
+      for (int j = 0; j < K; ++j) r_ex[j] = e[j] > R(0) ? N::flog(e[j]) - lme : N::ninf();
+      rho_ex = eo + (double)lme;
+    } else {
+#pragma unroll
+      for (int j = 0; j < K; ++j) r_ex[j] = R(0);
+      rho_ex = -CUDART_INF;
+    }
+  }
+
+  // Row-major base of this warp's alpha store.
+  R* aw = kGlobal ? reinterpret_cast<R*>(a.alpha_ws) + (start + t0) * K : abuf + lane * a.a_pitch;
+  const bool vec_ok = ((start * K * (int64_t)sizeof(R)) % 16 == 0) &&
+                      ((L * K * (int)sizeof(R)) % 16 == 0);
+
+  // ---- phase 3a: forward re-sweep -----------------------------------------
+  R* __restrict__ outA = reinterpret_cast<R*>(a.log_alpha);
+  {
+    R av[K];
+    double lam = lam_in;
+#pragma unroll
+    for (int j = 0; j < K; ++j) av[j] = a_in[j];
+#pragma unroll 1
+    for (int s = 0; s < L; ++s) {
+      const int t = t0 + s;
+      if (s < len) {
+        ObsFeat<R> f0, f1;
+        R lb[K], u[K];
+        em.eval(yat0(s), yat1(s), f0, f1, lb, oob);
+        if (t == 0) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) u[j] = lpi[j] + lb[j];
+          lam = 0.0;
+        } else {
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            R acc = av[0] * Am[0][c];
+#pragma unroll
+            for (int i = 1; i < K; ++i) acc = fma(av[i], Am[i][c], acc);
+            u[c] = N::flog(acc) + lb[c];
+          }
+        }
+        if (outA) {
+          const R lr = (R)lam;
+          R o[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) o[j] = lr + u[j];
+          VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
+        }
+        R M = u[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) M = rmax(M, u[j]);
+        if (M > N::ninf()) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) av[j] = N::fexp(u[j] - M);
+          lam += (double)M;
+        } else {
+#pragma unroll
+          for (int j = 0; j < K; ++j) av[j] = R(0);
+        }
+        VecIO<R, K>::st(aw + s * (kGlobal ? K : K), av);
+      }
+      if (outA && ((s % kSlab) == kSlab - 1 || s == L - 1)) {
+        __syncwarp();
+        flush_slab<R, K>(outA, stA, a.s_pitch, start, L, T, s - (s % kSlab), lane, vec_ok);
+        __syncwarp();
+      }
+    }
+  }
+  if (kGlobal) __syncwarp();
+
+  // ---- phase 3b: backward re-sweep with posteriors and statistics --------
+  R* __restrict__ outB = reinterpret_cast<R*>(a.log_beta);
+  R* __restrict__ outG = reinterpret_cast<R*>(a.gamma);
+  R* __restrict__ outX = reinterpret_cast<R*>(a.xi);
+  R X[K][K];
+  R gtot[K], g0[K];
+  R st[TR::S][K][LOGHMM_NSLOT];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    gtot[i] = R(0);
+    g0[i] = R(0);
+#pragma unroll
+    for (int j = 0; j < K; ++j) X[i][j] = R(0);
+#pragma unroll
+    for (int s = 0; s < TR::S; ++s)
+#pragma unroll
+      for (int q = 0; q < LOGHMM_NSLOT; ++q) st[s][i][q] = R(0);
+  }
+  {
+    R r[K];
+    double rho = rho_ex;
+#pragma unroll
+    for (int j = 0; j < K; ++j) r[j] = r_ex[j];
+    const int s_top = len - 1;
+    // Emission of the step above the current pair, carried between iterations
+    // so every step is evaluated once.
+    ObsFeat<R> cf0, cf1;
+    R clb[K];
+#pragma unroll 1
+    for (int s = L - 1; s >= -1; --s) {
+      if (len > 0 && s == s_top) {
+        // last step of the chunk: beta from the scan
+        const int t = t0 + s;
+        em.eval(yat0(s), yat1(s), cf0, cf1, clb, oob);
+        R q[K], av[K], g[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) q[j] = N::fexp(r[j]);
+        VecIO<R, K>::ld(aw + s * K, av);
+        R Z = R(0);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          g[j] = av[j] * q[j];
+          Z += g[j];
+        }
+        const R iz = R(1) / Z;
+#pragma unroll
+        for (int j = 0; j < K; ++j) g[j] *= iz;
+        if (outB) {
+          const R rr = (R)rho;
+          R o[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) o[j] = rr + r[j];
+          VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
+        }
+        if (outG) VecIO<R, K>::st(stB + lane * a.s_pitch + (s % kSlab) * K, g);
+        stats_step<R, K, CFG>(st, g, em, cf0, cf1);
+        if (t < T - 1) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) gtot[j] += g[j];
+        }
+        if (t == 0) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) g0[j] = g[j];
+        }
+      } else if (len > 0 && s < s_top && (t0 + s) >= 0) {
+        // pair (t0+s, t0+s+1); clb holds log b at t0+s+1
+        const int tl = t0 + s;
+        R u[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) u[j] = clb[j] + r[j];
+        R M = u[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) M = rmax(M, u[j]);
+        const bool fin = M > N::ninf();
+        R w[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) w[j] = fin ? N::fexp(u[j] - M) : R(0);
+        R q[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          R acc = Am[i][0] * w[0];
+#pragma unroll
+          for (int j = 1; j < K; ++j) acc = fma(Am[i][j], w[j], acc);
+          q[i] = acc;
+        }
+        R ap[K];
+        if (s >= 0) {
+          VecIO<R, K>::ld(aw + s * K, ap);
+        } else {
+#pragma unroll
+          for (int j = 0; j < K; ++j) ap[j] = a_in[j];
+        }
+        R Z = R(0);
+#pragma unroll
+        for (int i = 0; i < K; ++i) Z = fma(ap[i], q[i], Z);
+        const R iz = R(1) / Z;
+        R ai[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) ai[i] = ap[i] * iz;
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+#pragma unroll
+          for (int j = 0; j < K; ++j) X[i][j] = fma(ai[i], w[j], X[i][j]);
+        if (outX) {
+          R* xr = outX + ((start - b) + tl) * (int64_t)(K * K);
+#pragma unroll
+          for (int i = 0; i < K; ++i)
+#pragma unroll
+            for (int j = 0; j < K; ++j) xr[i * K + j] = ai[i] * Am[i][j] * w[j];
+        }
+        R lq[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) lq[i] = q[i] > R(0) ? N::flog(q[i]) : N::ninf();
+        if (s >= 0) {
+          if (outB) {
+            const R rr = (R)(rho + (fin ? (double)M : 0.0));
+            R o[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) o[j] = rr + lq[j];
+            VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
+          }
+          R g[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) g[j] = ai[j] * q[j];
+          if (outG) VecIO<R, K>::st(stB + lane * a.s_pitch + (s % kSlab) * K, g);
+          em.eval(yat0(s), yat1(s), cf0, cf1, clb, oob);
+          stats_step<R, K, CFG>(st, g, em, cf0, cf1);
+#pragma unroll
+          for (int j = 0; j < K; ++j) gtot[j] += g[j];
+          if (tl == 0) {
+#pragma unroll
+            for (int j = 0; j < K; ++j) g0[j] = g[j];
+          }
+        }
+        R mq = lq[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) mq = rmax(mq, lq[j]);
+        if (mq > N::ninf()) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) r[j] = lq[j] - mq;
+          rho += (fin ? (double)M : 0.0) + (double)mq;
+        }
+      }
+      if (s >= 0 && (s % kSlab) == 0 && (outB || outG)) {
+        __syncwarp();
+        if (outB) flush_slab<R, K>(outB, stA, a.s_pitch, start, L, T, s, lane, vec_ok);
+        if (outG) flush_slab<R, K>(outG, stB, a.s_pitch, start, L, T, s, lane, vec_ok);
+        __syncwarp();
+      }
+    }
+  }
+
+  // ---- reductions and per-sequence outputs --------------------------------
+  const int dead_all = (int)warp_min_ll((long long)dead_t);
+  const unsigned nanb = __ballot_sync(kFull, nan_seen);
+  const unsigned oobb = __ballot_sync(kFull, oob);
+  if (lane == 0) {
+    a.ll[b] = LL;
+    if (a.flags) {
+      a.flags[2 * b] = dead_all == INT_MAX ? -1 : (int64_t)dead_all;
+      a.flags[2 * b + 1] = (nanb ? 1 : 0) | (oobb ? 2 : 0);
+    }
+  }
+  if (a.partials) {
+    double* row = a.partials + b * a.stats_width;
+    int idx = 0;
+    // xi totals: multiply by A after the lane reduction
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const R v = warp_sum(X[i][j]);
+        if (lane == (idx & 31)) row[idx] = (double)v * (double)Am[i][j];
+        ++idx;
+      }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const R v = warp_sum(gtot[j]);
+      if (lane == (idx & 31)) row[idx] = (double)v;
+      ++idx;
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const R v = __shfl_sync(kFull, g0[j], 0);
+      if (lane == (idx & 31)) row[idx] = (double)v;
+      ++idx;
+    }
+#pragma unroll
+    for (int s = 0; s < TR::S; ++s)
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int q = 0; q < LOGHMM_NSLOT; ++q) {
+          const int ns = s == 0 ? TR::NS0 : TR::NS1;
+          R v = R(0);
+          if (q < ns) v = warp_sum(st[s][j][q]);
+          if (lane == (idx & 31)) row[idx] = (double)v;
+          ++idx;
+        }
+    // pad the unused second stream
+    for (; idx < a.stats_width; ++idx)
+      if (lane == (idx & 31)) row[idx] = 0.0;
+  }
+}
+
+}  // namespace lhmm

@@ -1,0 +1,321 @@
+// hmm_large.cuh — forward-backward and Viterbi for 8 < K <= 64 (config 5).
+//
+// One CTA per sequence, one thread per state.  The transition matrix is
+// staged once in shared memory; the state vector is exchanged through shared
+// memory with one barrier per step.  This is the straightforward sequential
+// sweep over T (inference.py:129-146, 191-210); the parallel-over-T scan of
+// hmm_fb.cuh costs K^3 per step and does not pay at K=64.
+#pragma once
+
+#include "hmm_common.cuh"
+#include "hmm_fb.cuh"
+#include "hmm_viterbi.cuh"
+
+namespace lhmm {
+
+template <typename R>
+__device__ __forceinline__ R block_max(R v, R* red, int nw) {
+  v = warp_max(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  R m = red[0];
+  for (int i = 1; i < nw; ++i) m = rmax(m, red[i]);
+  return m;
+}
+
+template <typename R>
+__device__ __forceinline__ R block_sum(R v, R* red, int nw) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  R m = red[0];
+  for (int i = 1; i < nw; ++i) m += red[i];
+  return m;
+}
+
+// Runtime-K version of the fast emission for state j.
+template <typename R>
+__device__ __forceinline__ R large_logb(const EmP<R>& p0, const EmP<R>& p1, bool two, R y0, R y1,
+                                        const double* lut, int lut_n, bool& oob,
+                                        ObsFeat<R>& f0, ObsFeat<R>& f1) {
+  obs_features<R, kCfgMixed>(f0, y0, lut, lut_n, oob, 1 << p0.fam);
+  R v = fast_logb_rt<R>(p0, f0);
+  if (two) {
+    obs_features<R, kCfgMixed>(f1, y1, lut, lut_n, oob, 1 << p1.fam);
+    v += fast_logb_rt<R>(p1, f1);
+  }
+  return v;
+}
+
+// blockDim.x = 32 * ceil(K/32); thread j < K owns state j.
+template <typename R>
+__global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
+  typedef Num<R> N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* As = reinterpret_cast<R*>(smem_raw);  // K*K
+  R* av = As + K * K;                      // K (current vector)
+  R* red = av + K;                         // 32
+  const int tid = threadIdx.x;
+  const int nw = blockDim.x >> 5;
+  const int64_t b = blockIdx.x;
+  if (b >= a.B) return;
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  const bool act = tid < K;
+  const int j = act ? tid : 0;
+  const loghmm_model_t* md = a.model;
+  for (int e = tid; e < K * K; e += blockDim.x) As[e] = (R)md->A[e];
+  const EmP<R> p0 = load_emission<R>(md->em[0][j]);
+  EmP<R> p1;
+  const bool two = a.n_streams > 1;
+  if (two) p1 = load_emission<R>(md->em[1][j]);
+  else p1.fam = LOGHMM_FAM_NONE;
+  const R lpi = (R)md->log_pi[j];
+  const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  R* aws = reinterpret_cast<R*>(a.alpha_ws) + start * K;  // [T, K] normalised alpha
+  R* outA = a.log_alpha ? reinterpret_cast<R*>(a.log_alpha) + start * K : nullptr;
+  R* outB = a.log_beta ? reinterpret_cast<R*>(a.log_beta) + start * K : nullptr;
+  R* outG = a.gamma ? reinterpret_cast<R*>(a.gamma) + start * K : nullptr;
+  R* outX = a.xi ? reinterpret_cast<R*>(a.xi) + (start - b) * (int64_t)K * K : nullptr;
+  bool oob = false, nan_seen = false;
+  int dead_t = INT_MAX;
+  __syncthreads();
+
+  // forward
+  double lam = 0.0;
+  R a_j = R(0);
+  for (int t = 0; t < T; ++t) {
+    ObsFeat<R> f0, f1;
+    const R v0 = y0g[t], v1 = two ? y1g[t] : R(0);
+    if (isnan(v0) || isnan(v1)) nan_seen = true;
+    const R lb = act ? large_logb<R>(p0, p1, two, v0, v1, a.lut, a.lut_n, oob, f0, f1) : N::ninf();
+    R u;
+    if (t == 0) {
+      u = lpi + lb;
+    } else {
+      R acc = R(0);
+      for (int i = 0; i < K; ++i) acc = fma(av[i], As[i * K + j], acc);
+      u = (acc > R(0) ? N::flog(acc) : N::ninf()) + lb;
+    }
+    if (act && outA) outA[(int64_t)t * K + j] = (R)lam + u;
+    const R mlb = block_max(act ? lb : N::ninf(), red, nw);
+    if (!(mlb > N::ninf()) && t < dead_t) dead_t = t;
+    const R M = block_max(act ? u : N::ninf(), red, nw);
+    a_j = (M > N::ninf()) ? N::fexp(u - M) : R(0);
+    if (M > N::ninf()) lam += (double)M;
+    if (act) {
+      av[j] = a_j;
+      aws[(int64_t)t * K + j] = a_j;
+    }
+    __syncthreads();
+  }
+  double LL;
+  {
+    const R s = block_sum(act ? a_j : R(0), red, nw);
+    LL = s > R(0) ? lam + (double)N::flog(s) : -CUDART_INF;
+  }
+
+  // backward
+  R* wv = av;  // reuse: w vector
+  R gtot = R(0), g0 = R(0);
+  R st[2][LOGHMM_NSLOT];
+  for (int s = 0; s < 2; ++s)
+    for (int q = 0; q < LOGHMM_NSLOT; ++q) st[s][q] = R(0);
+  R* X = red + 32;  // K*K xi accumulators (column j owned by thread j)
+  for (int i = 0; i < K; ++i)
+    if (act) X[i * K + j] = R(0);
+  R r = R(0);  // log beta~ at current t (max 0)
+  double rho = 0.0;
+  for (int t = T - 1; t >= 0; --t) {
+    ObsFeat<R> f0, f1;
+    const R v0 = y0g[t], v1 = two ? y1g[t] : R(0);
+    const R lb = act ? large_logb<R>(p0, p1, two, v0, v1, a.lut, a.lut_n, oob, f0, f1) : N::ninf();
+    // gamma at t: a_t * exp(r)
+    const R at = act ? aws[(int64_t)t * K + j] : R(0);
+    const R q = act ? N::fexp(r) : R(0);
+    const R gz = block_sum(at * q, red, nw);
+    const R gj = at * q / gz;
+    if (act) {
+      if (outB) outB[(int64_t)t * K + j] = (R)rho + r;
+      if (outG) outG[(int64_t)t * K + j] = gj;
+      R accs[LOGHMM_NSLOT];
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[0][qq];
+      stat_acc_rt<R>(accs, gj, p0, f0);
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[0][qq] = accs[qq];
+      if (two) {
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[1][qq];
+        stat_acc_rt<R>(accs, gj, p1, f1);
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[1][qq] = accs[qq];
+      }
+      if (t < T - 1) gtot += gj;
+      if (t == 0) g0 = gj;
+    }
+    if (t == 0) break;
+    // step to t-1: u = lb_t + r; w = exp(u - M); q_{t-1} = A w
+    const R u = act ? lb + r : N::ninf();
+    const R M = block_max(u, red, nw);
+    const bool fin = M > N::ninf();
+    const R w = (act && fin) ? N::fexp(u - M) : R(0);
+    if (act) wv[j] = w;
+    __syncthreads();
+    R acc = R(0);
+    if (act)
+      for (int jj = 0; jj < K; ++jj) acc = fma(As[j * K + jj], wv[jj], acc);
+    // xi_{t-1}(i, j) = a_{t-1}[i] A_ij w_j / Z, Z = sum_i a_{t-1}[i] q_i
+    const R ap = act ? aws[(int64_t)(t - 1) * K + j] : R(0);
+    const R Z = block_sum(ap * acc, red, nw);
+    const R iz = R(1) / Z;
+    // thread j (as column) accumulates X[i][j] += a_i/Z * w_j
+    if (act) {
+      for (int i = 0; i < K; ++i) {
+        const R ai = aws[(int64_t)(t - 1) * K + i] * iz;
+        X[i * K + j] = fma(ai, w, X[i * K + j]);
+        if (outX) outX[((int64_t)(t - 1) * K + i) * K + j] = ai * As[i * K + j] * w;
+      }
+    }
+    const R lq = acc > R(0) ? N::flog(acc) : N::ninf();
+    const R mq = block_max(act ? lq : N::ninf(), red, nw);
+    if (mq > N::ninf()) {
+      r = lq - mq;
+      rho += (fin ? (double)M : 0.0) + (double)mq;
+    }
+    // note: log_beta[t-1] = rho_prev + M + lq  ==  (rho + r) after the update
+    __syncthreads();
+  }
+  __syncthreads();
+  const int tid0 = tid;
+  // reductions into the partials row
+  if (a.partials) {
+    double* row = a.partials + b * a.stats_width;
+    if (act) {
+      for (int i = 0; i < K; ++i) row[i * K + j] = (double)X[i * K + j] * (double)As[i * K + j];
+      row[K * K + j] = (double)gtot;
+      row[K * K + K + j] = (double)g0;
+      for (int s = 0; s < 2; ++s)
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq)
+          row[K * K + 2 * K + (s * K + j) * LOGHMM_NSLOT + qq] = (double)st[s][qq];
+    }
+  }
+  // dead / nan flags
+  __shared__ int s_dead, s_nan, s_oob;
+  if (tid0 == 0) {
+    s_dead = INT_MAX;
+    s_nan = 0;
+    s_oob = 0;
+  }
+  __syncthreads();
+  if (dead_t != INT_MAX) atomicMin(&s_dead, dead_t);
+  if (nan_seen) s_nan = 1;
+  if (oob) s_oob = 1;
+  __syncthreads();
+  if (tid0 == 0) {
+    a.ll[b] = LL;
+    if (a.flags) {
+      a.flags[2 * b] = s_dead == INT_MAX ? -1 : s_dead;
+      a.flags[2 * b + 1] = (s_nan ? 1 : 0) | (s_oob ? 2 : 0);
+    }
+  }
+}
+
+// Viterbi, one CTA per sequence, thread j = destination state.  Backpointers
+// go to a byte table in the workspace; thread 0 walks the path with blocks of
+// backpointer rows prefetched into shared memory.
+template <typename R>
+__global__ void __launch_bounds__(64) viterbi_large_kernel(const VitArgs a, int K,
+                                                           uint8_t* backws) {
+  typedef Num<R> N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* LA = reinterpret_cast<R*>(smem_raw);  // K*K log A
+  R* dv = LA + K * K;                      // K
+  uint8_t* bblk = reinterpret_cast<uint8_t*>(dv + K);  // 256*K bytes
+  __shared__ int s_cur;
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  if (b >= a.B) return;
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  const bool act = tid < K;
+  const int j = act ? tid : 0;
+  const loghmm_model_t* md = a.model;
+  for (int e = tid; e < K * K; e += blockDim.x) LA[e] = (R)md->log_A[e];
+  const loghmm_emission_t e0 = md->em[0][j];
+  loghmm_emission_t e1;
+  const bool two = a.n_streams > 1;
+  if (two) e1 = md->em[1][j];
+  const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  uint8_t* bk = backws + start * K;
+  bool oob = false;
+  auto logb = [&](int t) -> R {
+    R v = exact_logb<R>(e0, y0g[t], a.lut, a.lut_n, oob);
+    if (two) v = N::add(v, exact_logb<R>(e1, y1g[t], a.lut, a.lut_n, oob));
+    return v;
+  };
+  R delta = act ? N::add((R)md->log_pi[j], logb(0)) : N::ninf();
+  if (act) {
+    dv[j] = delta;
+    bk[j] = 0;
+    if (a.back) a.back[start * K + j] = 0;
+  }
+  __syncthreads();
+  for (int t = 1; t < T; ++t) {
+    R lb = act ? logb(t) : R(0);
+    R best = N::ninf();
+    int bi = 0;
+    if (act) {
+      best = N::add(dv[0], LA[j]);
+      for (int i = 1; i < K; ++i) {
+        const R c = N::add(dv[i], LA[i * K + j]);
+        if (c > best) {
+          best = c;
+          bi = i;
+        }
+      }
+    }
+    __syncthreads();
+    if (act) {
+      delta = N::add(best, lb);
+      dv[j] = delta;
+      bk[(int64_t)t * K + j] = (uint8_t)bi;
+      if (a.back) a.back[(start + t) * K + j] = (uint8_t)bi;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    R bv = dv[0];
+    int bi = 0;
+    for (int i = 1; i < K; ++i)
+      if (dv[i] > bv) {
+        bv = dv[i];
+        bi = i;
+      }
+    a.log_joint[b] = (double)bv;
+    s_cur = bi;
+  }
+  __syncthreads();
+  __threadfence_block();
+  // backtrace in blocks of 256 rows, walking down
+  constexpr int BLK = 256;
+  for (int hi = T - 1; hi >= 0; hi -= BLK) {
+    const int lo = max(0, hi - BLK + 1);
+    const int rows = hi - lo + 1;
+    for (int e = tid; e < rows * K; e += blockDim.x) bblk[e] = bk[(int64_t)lo * K + e];
+    __syncthreads();
+    if (tid == 0) {
+      int cur = s_cur;
+      for (int t = hi; t >= lo; --t) {
+        a.path[start + t] = cur;
+        if (t >= 1) cur = bblk[(t - lo) * K + cur];
+      }
+      s_cur = cur;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace lhmm

@@ -1,0 +1,70 @@
+// hmm_launch.cuh — host-side launch templates, explicitly instantiated per
+// (dtype, K) in inst_*.cu so the heavy kernel bodies compile in parallel.
+#pragma once
+
+#include "hmm_fb.cuh"
+#include "hmm_viterbi.cuh"
+
+namespace lhmm {
+
+template <typename R, int K, int CFG, bool G>
+static cudaError_t launch_fb_one(const FBArgs& a, dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t st) {
+  auto fn = fb_small_kernel<R, K, CFG, G>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<grid, block, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename R, int K, bool G>
+static cudaError_t launch_fb_cfg(const FBArgs& a, int cfg, dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t st) {
+  switch (cfg) {
+    case kCfgGauss: return launch_fb_one<R, K, kCfgGauss, G>(a, grid, block, smem, st);
+    case kCfgStudent: return launch_fb_one<R, K, kCfgStudent, G>(a, grid, block, smem, st);
+    case kCfgGamma: return launch_fb_one<R, K, kCfgGamma, G>(a, grid, block, smem, st);
+    case kCfgVonMises: return launch_fb_one<R, K, kCfgVonMises, G>(a, grid, block, smem, st);
+    case kCfgPoisson: return launch_fb_one<R, K, kCfgPoisson, G>(a, grid, block, smem, st);
+    case kCfgGammaVM: return launch_fb_one<R, K, kCfgGammaVM, G>(a, grid, block, smem, st);
+    default: return launch_fb_one<R, K, kCfgMixed, G>(a, grid, block, smem, st);
+  }
+}
+
+template <typename R, int K>
+cudaError_t launch_fb_small(const FBArgs& a, int cfg, bool global, dim3 grid, dim3 block,
+                            size_t smem, cudaStream_t st) {
+  return global ? launch_fb_cfg<R, K, true>(a, cfg, grid, block, smem, st)
+                : launch_fb_cfg<R, K, false>(a, cfg, grid, block, smem, st);
+}
+
+template <typename R, int K>
+cudaError_t launch_vit_small(const VitArgs& a, bool global, dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st) {
+  if (global) {
+    auto fn = viterbi_small_kernel<R, K, true>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, block, smem, st>>>(a);
+  } else {
+    auto fn = viterbi_small_kernel<R, K, false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, block, smem, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+#define LHMM_DECLARE_INST(R, K)                                                              \
+  template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \
+                                             cudaStream_t);                                  \
+  template cudaError_t launch_vit_small<R, K>(const VitArgs&, bool, dim3, dim3, size_t,      \
+                                              cudaStream_t);
+
+#define LHMM_EXTERN_INST(R, K)                                                                      \
+  extern template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \
+                                                    cudaStream_t);                                  \
+  extern template cudaError_t launch_vit_small<R, K>(const VitArgs&, bool, dim3, dim3, size_t,      \
+                                                     cudaStream_t);
+
+}  // namespace lhmm

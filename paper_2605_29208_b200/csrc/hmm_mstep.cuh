@@ -1,0 +1,486 @@
+// hmm_mstep.cuh — deterministic statistics reduction and the per-state
+// scalar M-step kernels (one thread per state).
+//
+// Device ports of the reference's scalar math:
+//   special.py:81-128  digamma / trigamma (recurrence to x>=10 + asymptotic series)
+//   special.py:135-217 two-branch A&S Bessel I0/I1, log I0, I1/I0 ratio
+//   distributions.py:732-761 _newton_1d (safeguarded bracketed Newton)
+//   distributions.py:632-636 fit_gaussian, :658-663 fit_poisson,
+//                    :764-786 fit_gamma_nr, :874-916 fit_vonmises,
+//                    :1031-1076 fit_student_t_ecme (E-step sums, CM-1, nu Newton)
+//   training.py:105-127 m_step_transitions, :130-148 collapse guard
+// The ECME likelihood guard (distributions.py:1080-1086) needs a data pass
+// and lives in student_guard_kernel below.
+#pragma once
+
+#include "hmm_common.cuh"
+
+namespace lhmm {
+
+// ---- special functions (special.py) -----------------------------------------
+__device__ inline double sp_digamma(double x) {
+  double acc = 0.0;
+  while (x < 10.0) {
+    acc -= 1.0 / x;
+    x += 1.0;
+  }
+  const double inv = 1.0 / x, inv2 = inv * inv;
+  const double series =
+      log(x) - 0.5 * inv -
+      inv2 * (1.0 / 12.0 -
+              inv2 * (1.0 / 120.0 - inv2 * (1.0 / 252.0 - inv2 * (1.0 / 240.0 - inv2 / 132.0))));
+  return acc + series;
+}
+
+__device__ inline double sp_trigamma(double x) {
+  double acc = 0.0;
+  while (x < 10.0) {
+    acc += 1.0 / (x * x);
+    x += 1.0;
+  }
+  const double inv = 1.0 / x, inv2 = inv * inv;
+  const double series =
+      inv * (1.0 + inv * (0.5 + inv * (1.0 / 6.0 -
+                                       inv2 * (1.0 / 30.0 -
+                                               inv2 * (1.0 / 42.0 -
+                                                       inv2 * (1.0 / 30.0 - 5.0 * inv2 / 66.0))))));
+  return acc + series;
+}
+
+__constant__ double kI0S[7] = {1.0, 3.5156229, 3.0899424, 1.2067492, 0.2659732, 0.0360768, 0.0045813};
+__constant__ double kI0L[9] = {0.39894228, 0.01328592, 0.00225319, -0.00157565, 0.00916281,
+                               -0.02057706, 0.02635537, -0.01647633, 0.00392377};
+__constant__ double kI1S[7] = {0.5, 0.87890594, 0.51498869, 0.15084934, 0.02658733, 0.00301532, 0.00032411};
+__constant__ double kI1L[9] = {0.39894228, -0.03988024, -0.00362018, 0.00163801, -0.01031555,
+                               0.02282967, -0.02895312, 0.01787654, -0.00420059};
+
+__device__ inline double sp_poly(const double* c, int n, double u) {
+  double acc = 0.0;
+  for (int i = n - 1; i >= 0; --i) acc = acc * u + c[i];
+  return acc;
+}
+__device__ inline double sp_bessel_i0(double x) {
+  if (x <= 3.75) {
+    const double t = x / 3.75;
+    return sp_poly(kI0S, 7, t * t);
+  }
+  return exp(x) / sqrt(x) * sp_poly(kI0L, 9, 3.75 / x);
+}
+__device__ inline double sp_bessel_i1(double x) {
+  if (x <= 3.75) {
+    const double t = x / 3.75;
+    return x * sp_poly(kI1S, 7, t * t);
+  }
+  return exp(x) / sqrt(x) * sp_poly(kI1L, 9, 3.75 / x);
+}
+__device__ inline double sp_log_bessel_i0(double x) {
+  if (x <= 3.75) {
+    const double t = x / 3.75;
+    return log(sp_poly(kI0S, 7, t * t));
+  }
+  return x - 0.5 * log(x) + log(sp_poly(kI0L, 9, 3.75 / x));
+}
+__device__ inline double sp_i1_i0_ratio(double k) {
+  if (k == 0.0) return 0.0;
+  if (k <= 3.75) return sp_bessel_i1(k) / sp_bessel_i0(k);
+  const double u = 3.75 / k;
+  return sp_poly(kI1L, 9, u) / sp_poly(kI0L, 9, u);
+}
+
+constexpr double kLog2Pi = 1.8378770664093453;  // math.log(2*pi)
+constexpr double kScaleFloor = 1e-9;             // distributions.py:73
+constexpr double kKappaCeiling = 1e5;            // distributions.py:74
+
+// Host-equivalent constants of a record (see loghmm_emission_t).
+__device__ inline void em_constants(loghmm_emission_t& e) {
+  switch (e.family) {
+    case LOGHMM_FAM_GAUSSIAN:
+      e.c[0] = (-0.5 * kLog2Pi) - log(e.p[1]);
+      break;
+    case LOGHMM_FAM_STUDENT_T: {
+      const double nu = e.p[2];
+      e.c[0] = lgamma((nu + 1.0) / 2.0) - lgamma(nu / 2.0) - 0.5 * log(nu * CUDART_PI) - log(e.p[1]);
+      e.c[1] = (nu + 1.0) / 2.0;
+      break;
+    }
+    case LOGHMM_FAM_GAMMA:
+      e.c[0] = e.p[0] * log(e.p[1]) - lgamma(e.p[0]);
+      e.c[1] = e.p[0] - 1.0;
+      break;
+    case LOGHMM_FAM_VON_MISES:
+      e.c[0] = kLog2Pi;
+      e.c[1] = sp_log_bessel_i0(e.p[1]);
+      break;
+    case LOGHMM_FAM_POISSON:
+      e.c[0] = log(e.p[0]);
+      break;
+    default:
+      break;
+  }
+}
+
+// _newton_1d (distributions.py:732-761) for the Gamma shape score.
+__device__ inline double gamma_newton(double c, double x0, bool& ok) {
+  double lo = 0.0, hi = CUDART_INF, x = x0;
+  for (int it = 0; it < 50; ++it) {
+    const double s = log(x) - sp_digamma(x) - c;
+    if (fabs(s) <= 1e-10) {
+      ok = true;
+      return x;
+    }
+    if (s > 0.0) lo = fmax(lo, x);
+    else hi = fmin(hi, x);
+    const double d = 1.0 / x - sp_trigamma(x);
+    double prop = d != 0.0 ? x - s / d : CUDART_INF;
+    if (!(isfinite(prop) && lo < prop && prop < hi)) prop = isinf(hi) ? x * 8.0 : 0.5 * (lo + hi);
+    x = prop;
+  }
+  ok = fabs(log(x) - sp_digamma(x) - c) <= 1e-10;
+  return x;
+}
+
+// Student-t nu objective / score / curvature (distributions.py:995-1009).
+__device__ inline double st_obj(double nu, double n, double mix) {
+  return n * (nu / 2.0 * log(nu / 2.0) - lgamma(nu / 2.0)) + nu / 2.0 * mix;
+}
+__device__ inline double st_score(double nu, double n, double mix) {
+  return n / 2.0 * (log(nu / 2.0) + 1.0 - sp_digamma(nu / 2.0)) + mix / 2.0;
+}
+__device__ inline double st_curv(double nu, double n) {
+  return n / 4.0 * (2.0 / nu - sp_trigamma(nu / 2.0));
+}
+
+// Deterministic reduction: totals[c] = sum_b partials[b, c] in a fixed tree,
+// totals[width] = sum_b ll[b].  One CTA per column block.
+__global__ void __launch_bounds__(256) reduce_stats_kernel(const double* __restrict__ partials,
+                                                           const double* __restrict__ ll,
+                                                           int64_t B, int64_t width,
+                                                           double* __restrict__ totals) {
+  __shared__ double red[256];
+  const int64_t col = blockIdx.x;  // 0..width (width = ll column)
+  double acc = 0.0;
+  for (int64_t b = threadIdx.x; b < B; b += blockDim.x)
+    acc += (col < width) ? partials[b * width + col] : ll[b];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[col] = red[0];
+}
+
+// guard_state layout per (stream, state): [mu, sigma, nu0, nu_cand, n, active, k_next, pad]
+constexpr int kGuardStride = 8;
+
+__global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const double* __restrict__ tot,
+                             int64_t nseq, double eps, double nu_ceiling, double nu_tol,
+                             int max_newton, loghmm_model_t* __restrict__ mout,
+                             int32_t* __restrict__ status, double* __restrict__ guard) {
+  const int K = min_->K;
+  const int S = min_->n_streams;
+  const int tid = threadIdx.x;
+  const int width_xi = K * K;
+  const double* xi = tot;
+  const double* gt = tot + width_xi;
+  const double* g0 = gt + K;
+  const double* em = g0 + K;
+  if (tid == 0) {
+    mout->K = K;
+    mout->n_streams = S;
+  }
+  // ---- transitions and initial distribution (training.py:105-127) ----
+  if (tid < K) {
+    const int i = tid;
+    double row[LOGHMM_MAX_STATES];
+    for (int j = 0; j < K; ++j) mout->A[i * K + j] = min_->A[i * K + j];
+    if (gt[i] >= eps) {
+      double total = 0.0;
+      for (int j = 0; j < K; ++j) {
+        row[j] = xi[i * K + j] / gt[i];
+        total += row[j];
+      }
+      if (total > 0.0)
+        for (int j = 0; j < K; ++j) mout->A[i * K + j] = row[j] / total;
+    }
+    for (int j = 0; j < K; ++j) {
+      const double v = mout->A[i * K + j];
+      mout->log_A[i * K + j] = v > 0.0 ? log(v) : -CUDART_INF;
+    }
+  }
+  if (tid == 0) {
+    double pis = 0.0;
+    for (int j = 0; j < K; ++j) pis += g0[j] / (double)nseq;
+    for (int j = 0; j < K; ++j) {
+      const double p = (g0[j] / (double)nseq) / pis;
+      mout->pi[j] = p;
+      mout->log_pi[j] = p > 0.0 ? log(p) : -CUDART_INF;
+    }
+  }
+  // ---- emissions (training.py:130-148 -> distributions.py:1094 refit) ----
+  for (int idx = tid; idx < S * K; idx += blockDim.x) {
+    const int s = idx / K, j = idx % K;
+    loghmm_emission_t e = min_->em[s][j];
+    const double* q = em + (size_t)(s * K + j) * LOGHMM_NSLOT;
+    const double n_state = em[(size_t)(0 * K + j) * LOGHMM_NSLOT + 0];  // total weight of state j
+    int32_t st = LOGHMM_MS_UPDATED;
+    double* gs = guard + (size_t)(s * K + j) * kGuardStride;
+    gs[5] = 0.0;
+    if (e.family == LOGHMM_FAM_NONE) {
+      // nothing
+    } else if (n_state < eps) {
+      st = LOGHMM_MS_COLLAPSED;
+    } else {
+      const double n = q[0];
+      switch (e.family) {
+        case LOGHMM_FAM_GAUSSIAN: {
+          const double d = q[1] / n;
+          double var = (q[2] - q[1] * d) / n;
+          if (var < 0.0) var = 0.0;
+          e.p[0] = e.p[0] + d;
+          e.p[1] = fmax(sqrt(var), kScaleFloor);
+          break;
+        }
+        case LOGHMM_FAM_POISSON: {
+          if (q[2] > 0.0) {
+            st = LOGHMM_MS_ERR_SUPPORT;
+            break;
+          }
+          e.p[0] = fmax(q[1] / n, kScaleFloor);
+          break;
+        }
+        case LOGHMM_FAM_GAMMA: {
+          if (q[4] > 0.0) {
+            st = LOGHMM_MS_ERR_SUPPORT;
+            break;
+          }
+          const double m_old = e.p[0] / e.p[1];
+          const double d = q[1] / n;
+          const double mean = m_old + d;
+          const double var = (q[2] - q[1] * d) / n;
+          if (var <= 0.0) {
+            st = LOGHMM_MS_ERR_GAMMA_VAR;
+            break;
+          }
+          const double c = log(mean) - q[3] / n;
+          if (c <= 0.0) {
+            st = LOGHMM_MS_ERR_GAMMA_GAP;
+            break;
+          }
+          const double seed = mean * mean / var;
+          bool ok = false;
+          double alpha = gamma_newton(c, seed, ok);
+          if (!ok) {
+            st |= LOGHMM_MS_WARN_NEWTON;
+            alpha = seed;
+          }
+          e.p[0] = alpha;
+          e.p[1] = alpha / mean;
+          break;
+        }
+        case LOGHMM_FAM_VON_MISES: {
+          if (q[3] > 0.0) {
+            st = LOGHMM_MS_ERR_NONFINITE;
+            break;
+          }
+          const double S_ = q[1], C_ = q[2];
+          double mu = atan2(S_, C_);
+          if (mu <= -CUDART_PI) mu = CUDART_PI;
+          const double rbar = hypot(S_, C_) / n;
+          double kappa;
+          if (rbar <= 1e-12) {
+            kappa = 0.0;
+          } else if (rbar >= 1.0 - 1e-12) {
+            st |= LOGHMM_MS_WARN_BOUNDARY;
+            kappa = kKappaCeiling;
+          } else {
+            kappa = rbar * (2.0 - rbar * rbar) / (1.0 - rbar * rbar);
+            bool conv = false;
+            for (int it = 0; it < 50; ++it) {
+              const double A_ = sp_i1_i0_ratio(kappa);
+              const double f = A_ - rbar;
+              if (fabs(f) <= 1e-10) {
+                conv = true;
+                break;
+              }
+              double step = f / (1.0 - A_ * A_ - A_ / kappa);
+              double prop = kappa - step;
+              while (prop <= 0.0) {
+                step *= 0.5;
+                prop = kappa - step;
+              }
+              kappa = prop;
+              if (kappa >= kKappaCeiling) {
+                kappa = kKappaCeiling;
+                st |= LOGHMM_MS_WARN_CEILING;
+                break;
+              }
+            }
+            if (!conv && kappa < kKappaCeiling)
+              if (fabs(sp_i1_i0_ratio(kappa) - rbar) > 1e-10) st |= LOGHMM_MS_WARN_NEWTON;
+          }
+          e.p[0] = mu;
+          e.p[1] = kappa;
+          break;
+        }
+        case LOGHMM_FAM_STUDENT_T: {
+          const double mu0 = e.p[0], nu0 = e.p[2];
+          const double swu = q[1];
+          const double dmu = q[2] / swu;
+          const double mu = mu0 + dmu;
+          double s2 = (q[3] - q[2] * dmu) / n;
+          if (s2 < 0.0) s2 = 0.0;
+          const double sigma = fmax(sqrt(s2), kScaleFloor);
+          const double half = (nu0 + 1.0) / 2.0;
+          const double mix = q[4] + n * (sp_digamma(half) - log(half));
+          double nu = nu0;
+          for (int it = 0; it < max_newton; ++it) {
+            const double sc = st_score(nu, n, mix);
+            const double h = st_curv(nu, n);
+            double step = -sc / h;
+            double prop = nu + step;
+            while (prop <= 0.0) {
+              step *= 0.5;
+              prop = nu + step;
+            }
+            const double qn = st_obj(nu, n, mix);
+            while (st_obj(prop, n, mix) < qn && fabs(step) > 1e-300) {
+              step *= 0.5;
+              prop = nu + step;
+            }
+            if (prop >= nu_ceiling) {
+              st |= LOGHMM_MS_WARN_CEILING;
+              nu = nu_ceiling;
+              break;
+            }
+            const double moved = fabs(prop - nu);
+            nu = prop;
+            if (moved < nu_tol) break;
+          }
+          e.p[0] = mu;
+          e.p[1] = sigma;
+          // nu stays nu0 until the guard pass picks the candidate
+          gs[0] = mu;
+          gs[1] = sigma;
+          gs[2] = nu0;
+          gs[3] = nu;
+          gs[4] = n;
+          gs[5] = 1.0;
+          gs[6] = 0.0;  // candidates consumed
+          st |= LOGHMM_MS_STUDENT_GUARD;
+          break;
+        }
+        default:
+          break;
+      }
+    }
+    if (st < 16) em_constants(e);
+    mout->em[s][j] = e;
+    status[idx] = st;
+  }
+}
+
+// Guard pass: for every active Student-t state j (stream `sidx`), partial sums
+// over observations of w * log1p(z^2 / nu_k) for nu_k in the candidate list
+// (k = 0 is the base nu0), z = (y - mu)/sigma at the new location/scale.
+// Candidate list: c_1 = nu_cand, c_{k+1} = nu0 + 0.5 (c_k - nu0)
+// (distributions.py:1081-1085).  Per-block partials, reduced by
+// guard_select_kernel in a fixed order.
+template <typename R>
+__global__ void __launch_bounds__(256) student_guard_kernel(const R* __restrict__ y,
+                                                            const R* __restrict__ gamma,
+                                                            int64_t N, int K, int sidx,
+                                                            const double* __restrict__ guard,
+                                                            int ncand, double* __restrict__ part) {
+  __shared__ double red[256];
+  for (int j = 0; j < K; ++j) {
+    const double* gs = guard + (size_t)(sidx * K + j) * kGuardStride;
+    if (gs[5] == 0.0) continue;
+    const double mu = gs[0], sigma = gs[1], nu0 = gs[2];
+    double cand[LOGHMM_GUARD_CANDIDATES];
+    cand[0] = nu0;
+    double c = gs[3];
+    const int k0 = (int)gs[6];
+    for (int k = 0; k < k0; ++k) c = nu0 + 0.5 * (c - nu0);
+    for (int k = 1; k < ncand; ++k) {
+      cand[k] = c;
+      c = nu0 + 0.5 * (c - nu0);
+    }
+    double acc[LOGHMM_GUARD_CANDIDATES];
+    for (int k = 0; k < ncand; ++k) acc[k] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const double w = (double)gamma[i * K + j];
+      if (w > 0.0) {
+        const double z = ((double)y[i] - mu) / sigma;
+        const double z2 = z * z;
+        for (int k = 0; k < ncand; ++k) acc[k] += w * log1p(z2 / cand[k]);
+      }
+    }
+    for (int k = 0; k < ncand; ++k) {
+      red[threadIdx.x] = acc[k];
+      __syncthreads();
+      for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0)
+        part[((size_t)blockIdx.x * K + j) * LOGHMM_GUARD_CANDIDATES + k] = red[0];
+      __syncthreads();
+    }
+  }
+}
+
+__device__ inline double st_ll(double n, double sum_l1p, double sigma, double nu) {
+  // sum_w [lg((nu+1)/2) - lg(nu/2) - 0.5 log(nu pi) - log sigma - (nu+1)/2 log1p(.)]
+  const double c = lgamma((nu + 1.0) / 2.0) - lgamma(nu / 2.0) - 0.5 * log(nu * CUDART_PI) - log(sigma);
+  return n * c - (nu + 1.0) / 2.0 * sum_l1p;
+}
+
+__global__ void guard_select_kernel(loghmm_model_t* __restrict__ mout, int K, int sidx,
+                                    double* __restrict__ guard, int ncand,
+                                    const double* __restrict__ part, int nblocks,
+                                    int32_t* __restrict__ status, int* __restrict__ need_more) {
+  const int j = threadIdx.x;
+  if (j >= K) return;
+  double* gs = guard + (size_t)(sidx * K + j) * kGuardStride;
+  if (gs[5] == 0.0) return;
+  double sums[LOGHMM_GUARD_CANDIDATES];
+  for (int k = 0; k < ncand; ++k) {
+    double s = 0.0;
+    for (int blk = 0; blk < nblocks; ++blk) s += part[((size_t)blk * K + j) * LOGHMM_GUARD_CANDIDATES + k];
+    sums[k] = s;
+  }
+  const double mu = gs[0], sigma = gs[1], nu0 = gs[2], n = gs[4];
+  const double base = st_ll(n, sums[0], sigma, nu0);
+  double c = gs[3];
+  const int k0 = (int)gs[6];
+  for (int k = 0; k < k0; ++k) c = nu0 + 0.5 * (c - nu0);
+  int chosen = -1;
+  for (int k = 1; k < ncand; ++k) {
+    if (k0 + k - 1 >= 60) break;
+    if (st_ll(n, sums[k], sigma, c) >= base - 1e-12) {
+      chosen = k;
+      break;
+    }
+    c = nu0 + 0.5 * (c - nu0);
+  }
+  loghmm_emission_t& e = mout->em[sidx][j];
+  if (chosen > 0) {
+    e.p[2] = c;
+    gs[5] = 0.0;
+  } else if (k0 + ncand - 1 >= 60) {
+    e.p[2] = nu0;  // for-else: fall back to nu0
+    gs[5] = 0.0;
+  } else {
+    gs[6] = (double)(k0 + ncand - 1);
+    atomicExch(need_more, 1);
+    return;
+  }
+  e.p[0] = mu;
+  e.p[1] = sigma;
+  em_constants(e);
+  status[sidx * K + j] &= ~LOGHMM_MS_STUDENT_GUARD;
+}
+
+}  // namespace lhmm

@@ -1,0 +1,279 @@
+// hmm_viterbi.cuh — batched Viterbi with compact backpointers and an
+// on-device backtrace, K <= 8.
+//
+// Reference: inference.py:191-210.  The max-plus recursion is evaluated in
+// exactly the reference's operation order so the backpointers and the path
+// are bit-identical:
+//   cand   = score[:, None] + log_a            (one IEEE add per candidate)
+//   back_t = argmax(cand, axis=0)              (first maximal index)
+//   score  = cand[back_t, j] + log_b[t, j]     (one IEEE add)
+// Because every value depends on the exact rounding of its predecessor, the
+// recursion is sequential in t; parallelism is B x K: K lanes per sequence
+// (lane j computes state j), 32/K sequences per warp, the previous score
+// vector exchanged with warp shuffles.
+//
+// Backpointers are stored as ceil(log2 K) ballot bit-planes per step (bit
+// g*K+j of plane p = bit p of back_t[j] of group g): K=4 costs 1 byte per
+// (sequence, step).  The backtrace then runs with all 32 lanes on one
+// sequence at a time: each lane composes the backpointer maps of its chunk,
+// a suffix scan of the composed maps (warp shuffles) gives every chunk its end
+// state, and each lane re-walks its chunk writing the path through a shared
+// memory staging buffer (coalesced int64 stores).
+#pragma once
+
+#include "hmm_common.cuh"
+
+namespace lhmm {
+
+struct VitArgs {
+  const loghmm_model_t* model;
+  const void* y0;
+  const void* y1;
+  const int64_t* offsets;
+  int64_t B;
+  const double* lut;
+  int lut_n;
+  int n_streams;
+  int64_t* path;
+  double* log_joint;
+  uint8_t* back;
+  uint32_t* planes_ws;  // global plane store (kGlobal): [warps][plane_words]
+  int64_t plane_words;  // per warp (= max_T * NP rounded)
+  int warp_smem_words;  // shared words per warp
+  int64_t* flags;
+};
+
+constexpr int kPathSlab = 8;
+constexpr int kPathPitch = 9;  // int64 elements, odd => conflict-free
+
+template <int K>
+struct Bits {
+  static constexpr int NP = K <= 1 ? 0 : K <= 2 ? 1 : K <= 4 ? 2 : 3;
+};
+
+// First-index argmax over cand[lo, hi) as a pairwise tree (the right half wins
+// only on a strictly greater value, which preserves numpy's tie rule).
+template <typename R, int LO, int HI>
+struct ArgMax {
+  static __device__ __forceinline__ void run(const R* c, R& v, int& i) {
+    if constexpr (HI - LO == 1) {
+      v = c[LO];
+      i = LO;
+    } else {
+      constexpr int MID = LO + (HI - LO + 1) / 2;
+      R lv, rv;
+      int li, ri;
+      ArgMax<R, LO, MID>::run(c, lv, li);
+      ArgMax<R, MID, HI>::run(c, rv, ri);
+      const bool right = rv > lv;
+      v = right ? rv : lv;
+      i = right ? ri : li;
+    }
+  }
+};
+
+__device__ __forceinline__ unsigned nib(unsigned m, unsigned e) { return (m >> (4 * e)) & 0xFu; }
+
+// back_t[v] for group gshift (= g*K) from the bit-planes of step t.
+template <int NP>
+__device__ __forceinline__ unsigned plane_lookup(const unsigned (&pl)[NP > 0 ? NP : 1], unsigned v) {
+  unsigned r = 0;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) r |= ((pl[p] >> v) & 1u) << p;
+  return r;
+}
+
+template <typename R, int K, bool kGlobal>
+__global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
+  typedef Num<R> N;
+  constexpr int G = kWarp / K;
+  constexpr int NP = Bits<K>::NP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const int g = lane / K;
+  const int j = lane - g * K;
+  const int64_t b = warp_id * G + g;
+  const bool valid = (g < G) && (b < a.B);
+  if (warp_id * G >= a.B) return;  // whole warp idle
+
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wib * a.warp_smem_words;
+  int64_t* pstage = reinterpret_cast<int64_t*>(wsm);  // kWarp * kPathPitch int64
+  uint32_t* planes = kGlobal ? a.planes_ws + warp_id * a.plane_words
+                             : wsm + 2 * kWarp * kPathPitch;
+
+  const loghmm_model_t* __restrict__ md = a.model;
+  const int64_t start = valid ? a.offsets[b] : 0;
+  const int T = valid ? (int)(a.offsets[b + 1] - start) : 0;
+  const R* __restrict__ y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const R* __restrict__ y1g = a.y1 ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  const bool two = a.n_streams > 1;
+
+  // column j of log A and the state's emission record
+  R la[K];
+  const int jj = valid ? j : 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) la[i] = (R)md->log_A[i * K + jj];
+  const loghmm_emission_t e0 = md->em[0][jj];
+  loghmm_emission_t e1;
+  if (two) e1 = md->em[1][jj];
+  bool oob = false;
+  auto logb = [&](int t) -> R {
+    const R v0 = y0g[t];
+    R v = exact_logb<R>(e0, v0, a.lut, a.lut_n, oob);
+    if (two) v = N::add(v, exact_logb<R>(e1, y1g[t], a.lut, a.lut_n, oob));
+    return v;
+  };
+
+  int Tmax = T;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) Tmax = max(Tmax, __shfl_xor_sync(kFull, Tmax, o));
+
+  // ---- forward max-plus recursion ---------------------------------------
+  R delta = N::ninf();
+  if (valid && T > 0) delta = N::add((R)md->log_pi[jj], logb(0));
+  if (valid && T > 0 && a.back) a.back[start * K + j] = 0;
+  unsigned pw[NP > 0 ? NP : 1];
+#pragma unroll
+  for (int p = 0; p < (NP > 0 ? NP : 1); ++p) pw[p] = 0;
+
+  constexpr int U = 8;
+  R ycur[U], ynx[U];
+  auto yload = [&](int t) -> R {
+    const int tt = t < T ? t : (T > 0 ? T - 1 : 0);
+    return valid && T > 0 ? y0g[tt] : R(0);
+  };
+#pragma unroll
+  for (int u = 0; u < U; ++u) ynx[u] = yload(1 + u);
+#pragma unroll 1
+  for (int tb = 1; tb < Tmax; tb += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) ycur[u] = ynx[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ynx[u] = yload(tb + U + u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = tb + u;
+      if (t < Tmax) {
+        const bool act = valid && t < T;
+        R lb;
+        {
+          R v = exact_logb<R>(e0, ycur[u], a.lut, a.lut_n, oob);
+          if (two) v = N::add(v, exact_logb<R>(e1, act ? y1g[t] : R(0), a.lut, a.lut_n, oob));
+          lb = v;
+        }
+        R cand[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) cand[i] = N::add(__shfl_sync(kFull, delta, g * K + i), la[i]);
+        R best;
+        int bi;
+        ArgMax<R, 0, K>::run(cand, best, bi);
+        const R nd = N::add(best, lb);
+        if (act) delta = nd;
+        const unsigned bpv = act ? (unsigned)bi : 0u;
+        if (act && a.back) a.back[(start + t) * K + j] = (uint8_t)bpv;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const unsigned w = __ballot_sync(kFull, (bpv >> p) & 1u);
+          if (lane == (t & 31)) pw[p] = w;
+        }
+        if ((t & 31) == 31 || t == Tmax - 1) {
+          const int tw = (t & ~31) + lane;
+          if (tw <= t) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) planes[(size_t)tw * NP + p] = pw[p];
+          }
+        }
+      }
+    }
+  }
+
+  // best final state per group (first index) and log joint
+  int best_last = 0;
+  R best_val = N::ninf();
+  {
+    R vals[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) vals[i] = __shfl_sync(kFull, delta, g * K + i);
+    ArgMax<R, 0, K>::run(vals, best_val, best_last);
+  }
+  if (valid && j == 0) {
+    a.log_joint[b] = (double)best_val;
+    if (a.flags && oob) a.flags[2 * b + 1] |= 2;
+  }
+  __syncwarp();
+  if (kGlobal) __threadfence_block();
+
+  // ---- backtrace, one sequence (group) at a time with all 32 lanes -------
+#pragma unroll 1
+  for (int gg = 0; gg < G; ++gg) {
+    const int64_t bb = warp_id * G + gg;
+    if (bb >= a.B) break;
+    const int Tg = __shfl_sync(kFull, T, gg * K);
+    const int64_t sg = __shfl_sync(kFull, start, gg * K);
+    const unsigned blast = (unsigned)__shfl_sync(kFull, best_last, gg * K);
+    if (Tg <= 0) continue;
+    const int L = (Tg + kWarp - 1) / kWarp;
+    const int t0 = lane * L;
+    const int t1 = min(t0 + L, Tg);
+    const unsigned gsh = (unsigned)(gg * K);
+    // compose the chunk's map: end state (t1-1) -> state at t0-1
+    unsigned F = 0x76543210u;
+#pragma unroll 1
+    for (int t = t1 - 1; t >= t0 && t >= 1; --t) {
+      unsigned pl[NP > 0 ? NP : 1];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) pl[p] = planes[(size_t)t * NP + p] >> gsh;
+      unsigned nf = 0;
+#pragma unroll
+      for (int e = 0; e < K; ++e) nf |= plane_lookup<NP>(pl, nib(F, e)) << (4 * e);
+      F = nf;
+    }
+    // inclusive suffix scan: H_c = F_c o F_{c+1} o ... o F_31
+    unsigned H = F;
+#pragma unroll
+    for (int d = 1; d < kWarp; d <<= 1) {
+      const unsigned Hn = __shfl_down_sync(kFull, H, d);
+      if (lane + d < kWarp) {
+        unsigned c = 0;
+#pragma unroll
+        for (int e = 0; e < K; ++e) c |= nib(H, nib(Hn, e)) << (4 * e);
+        H = c;
+      }
+    }
+    unsigned Hnext = __shfl_down_sync(kFull, H, 1);
+    if (lane == kWarp - 1) Hnext = 0x76543210u;
+    unsigned cur = nib(Hnext, blast);
+    // re-walk the chunk, staging the path in shared memory
+    int64_t* out = a.path + sg;
+#pragma unroll 1
+    for (int s = L - 1; s >= 0; --s) {
+      const int t = t0 + s;
+      if (t < t1) {
+        pstage[lane * kPathPitch + (s % kPathSlab)] = (int64_t)cur;
+        if (t >= 1) {
+          unsigned pl[NP > 0 ? NP : 1];
+#pragma unroll
+          for (int p = 0; p < NP; ++p) pl[p] = planes[(size_t)t * NP + p] >> gsh;
+          cur = plane_lookup<NP>(pl, cur);
+        }
+      }
+      if ((s % kPathSlab) == 0) {
+        __syncwarp();
+        // rows: lane-chunk c covers steps c*L + s .. +kPathSlab within [c*L, min(c*L+L,Tg))
+#pragma unroll
+        for (int rep = 0; rep < kPathSlab; ++rep) {
+          const int idx = rep * kWarp + lane;  // element index over 32 rows x 8
+          const int c = idx / kPathSlab, e = idx % kPathSlab;
+          const int tt = c * L + s + e;
+          if (s + e < L && tt < Tg) out[tt] = pstage[c * kPathPitch + e];
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+}  // namespace lhmm

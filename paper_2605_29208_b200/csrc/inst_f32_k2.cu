@@ -1,0 +1,5 @@
+// Explicit instantiation of the K<=8 kernels for dtype float, K=2.
+#include "hmm_launch.cuh"
+namespace lhmm {
+LHMM_DECLARE_INST(float, 2)
+}

@@ -1,0 +1,141 @@
+"""Preallocated batched pipeline: forward-backward + Viterbi + one
+Baum-Welch M-step over a fixed-shape batch (BASELINE metric workload).
+
+One ``run`` enqueues, on the caller's current stream:
+  fork:  stream A  loghmm_forward_backward (log_alpha, log_beta, gamma,
+                   per-sequence statistics)
+         stream B  loghmm_viterbi (path, log_joint)      -- runs concurrently
+  join:  loghmm_reduce_stats -> [optional all-reduce across ranks]
+         -> loghmm_mstep (-> loghmm_student_guard for Student-t states)
+No host synchronisation inside ``run``; ``fetch`` reads back the small
+results (total log-likelihood, the updated model block) like a user would.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native, engine
+from .inference import HmmModel
+from .training import TrainingConfig, model_from_record
+
+__all__ = ["Pipeline"]
+
+
+class Pipeline:
+    KERNELS_PER_RUN = 4  # fb, viterbi, reduce, mstep (+1 guard pass per Student-t stream)
+
+    def __init__(self, model: HmmModel, B: int, T: int, dtype="float32", *, outputs=True,
+                 config: TrainingConfig | None = None, process_group=None):
+        self.model = model
+        self.B, self.T = B, T
+        self.td = engine.torch_dtype(dtype)
+        self.ns = model.n_streams
+        self.config = config or TrainingConfig()
+        self.pg = process_group
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        K = model.num_states
+        self.K = K
+        N = B * T
+        off = np.arange(B + 1, dtype=np.int64) * T
+        self.y0 = torch.empty(N, dtype=self.td, device=dev)
+        self.y1 = torch.empty(N, dtype=self.td, device=dev) if self.ns == 2 else None
+        self.batch = engine.Batch(self.y0, self.y1, torch.from_numpy(off).to(dev), off, self.td)
+        self.dm = engine.DeviceModel.from_model(model, dev)
+        self.dm_next = engine.DeviceModel.empty_like(self.dm)
+        width = int(_native.lib().loghmm_stats_width(K, self.ns))
+        self.fb = engine.FBOutputs(
+            log_alpha=torch.empty((N, K), dtype=self.td, device=dev) if outputs else None,
+            log_beta=torch.empty((N, K), dtype=self.td, device=dev) if outputs else None,
+            gamma=torch.empty((N, K), dtype=self.td, device=dev),
+            xi=None,
+            ll=torch.empty(B, dtype=torch.float64, device=dev),
+            partials=torch.empty((B, width), dtype=torch.float64, device=dev),
+            flags=torch.empty((B, 2), dtype=torch.int64, device=dev),
+        )
+        self.vit = engine.VitOutputs(
+            path=torch.empty(N, dtype=torch.int64, device=dev),
+            log_joint=torch.empty(B, dtype=torch.float64, device=dev),
+            back=None,
+            flags=torch.zeros((B, 2), dtype=torch.int64, device=dev),
+        )
+        self.totals = torch.empty(width + 1, dtype=torch.float64, device=dev)
+        self.status = torch.zeros(self.ns * K, dtype=torch.int32, device=dev)
+        self.guard = torch.zeros(self.ns * K * 8, dtype=torch.float64, device=dev)
+        self.need_more = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ws_fb = engine.Workspace()
+        self.ws_vit = engine.Workspace()
+        self.s_fb = torch.cuda.Stream(device=dev)
+        self.s_vit = torch.cuda.Stream(device=dev)
+        fams = self.dm.host["em"]["family"]
+        self.student_streams = sorted({s for s in range(self.ns) for j in range(K)
+                                       if int(fams[s, j]) == _native.FAM["student_t"]})
+        # per-kernel CUDA events (recorded on the stream each kernel runs on)
+        self.ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for k in ("fb", "vit")}
+
+    @property
+    def kernels_per_run(self) -> int:
+        return self.KERNELS_PER_RUN + len(self.student_streams)
+
+    def load(self, y) -> None:
+        """Copy observations [B, T] (or [B, T, 2]) into the device batch."""
+        y = torch.as_tensor(y)
+        if self.ns == 1:
+            self.y0.copy_(y.reshape(-1), non_blocking=True)
+        else:
+            self.y0.copy_(y[..., 0].reshape(-1), non_blocking=True)
+            self.y1.copy_(y[..., 1].reshape(-1), non_blocking=True)
+
+    def run(self, time_kernels: bool = False) -> None:
+        main = torch.cuda.current_stream(self.dev)
+        self.s_fb.wait_stream(main)
+        self.s_vit.wait_stream(main)
+        with torch.cuda.stream(self.s_fb):
+            if time_kernels:
+                self.ev["fb"][0].record(self.s_fb)
+            engine.forward_backward(self.batch, self.dm, stats=True, out=self.fb, workspace=self.ws_fb)
+            if time_kernels:
+                self.ev["fb"][1].record(self.s_fb)
+        with torch.cuda.stream(self.s_vit):
+            if time_kernels:
+                self.ev["vit"][0].record(self.s_vit)
+            engine.viterbi(self.batch, self.dm, out=self.vit, workspace=self.ws_vit)
+            if time_kernels:
+                self.ev["vit"][1].record(self.s_vit)
+        main.wait_stream(self.s_fb)
+        main.wait_stream(self.s_vit)
+        engine.reduce_stats(self.fb.partials, self.fb.ll, self.totals)
+        if self.pg is not None:
+            import torch.distributed as dist
+
+            dist.all_reduce(self.totals, group=self.pg)
+        engine.mstep(self.dm, self.totals, self.B * (1 if self.pg is None else self._world()),
+                     self.config, self.dm_next, self.status, self.guard)
+        for s in self.student_streams:
+            engine.student_guard(self.batch, self.dm_next, self.fb.gamma, s, 2, self.guard,
+                                 self.status, self.need_more)
+
+    def _world(self) -> int:
+        import torch.distributed as dist
+
+        return dist.get_world_size(self.pg)
+
+    def kernel_ms(self) -> dict:
+        return {k: a.elapsed_time(b) for k, (a, b) in self.ev.items()}
+
+    def fetch(self):
+        """Small device->host read of the step's result: total log-likelihood
+        and the updated model."""
+        total = float(self.totals[-1].item())
+        rec = self.dm_next.to_host()
+        return total, rec
+
+    def updated_model(self) -> HmmModel:
+        return model_from_record(self.dm_next.to_host())
+
+    @property
+    def d2h_bytes(self) -> int:
+        return 8 + _native.MODEL_DTYPE.itemsize

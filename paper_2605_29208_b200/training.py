@@ -1,0 +1,319 @@
+"""Drop-in for the reference training layer (training.py), on B200.
+
+Baum-Welch keeps the reference's control flow and semantics
+(training.py:160-236): the trace holds the log-likelihood at the start of
+each iteration, convergence is |delta| < rel_tol*|LL| (or delta == 0), and the
+last iteration applies no M-step, so ``max_iterations=N`` runs N E-steps and
+N-1 M-steps.  Each E-step is one fused kernel over the whole batch
+(loghmm_forward_backward with statistics) plus a deterministic reduction;
+each M-step is one per-state kernel (loghmm_mstep) and, for Student-t
+states, the ECME likelihood-guard pass.  The model stays on the device
+between iterations; the host reads back only per-sequence flags and
+likelihoods (for the reference's error semantics) and the per-state status.
+"""
+
+from __future__ import annotations
+
+import math
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native, engine
+from .distributions import (
+    SCALE_FLOOR,
+    VONMISES_KAPPA_CEILING,
+    Distribution,
+    EcmeConfig,
+    FitWarning,
+    Gamma,
+    Gaussian,
+    Joint,
+    Poisson,
+    StudentT,
+    VonMises,
+    from_record,
+)
+from .inference import HmmModel
+
+__all__ = [
+    "TrainingConfig",
+    "TrainingReport",
+    "TrainingError",
+    "ModelScore",
+    "baum_welch",
+    "score_model",
+    "count_parameters",
+    "default_initial_model",
+]
+
+
+class TrainingError(ValueError):
+    """Raised when the data cannot be trained under the requested model."""
+
+
+@dataclass(frozen=True)
+class TrainingConfig:
+    """EM control knobs; defaults favor convergence over speed (training.py:46-61)."""
+
+    max_iterations: int = 500
+    rel_tol: float = 1e-8
+    collapse_epsilon: float = 1e-8
+    ecme: EcmeConfig = field(default_factory=EcmeConfig)
+
+    def __post_init__(self):
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be positive")
+        if not (0.0 < self.rel_tol < 1.0):
+            raise ValueError("rel_tol must lie in (0, 1)")
+        if self.collapse_epsilon <= 0.0:
+            raise ValueError("collapse_epsilon must be positive")
+
+
+@dataclass
+class TrainingReport:
+    log_likelihood_trace: list[float]
+    iterations: int
+    converged: bool
+    collapsed_states: list[tuple[int, int]]
+
+
+@dataclass(frozen=True)
+class ModelScore:
+    log_likelihood: float
+    num_params: int
+    num_obs: int
+    aic: float
+    bic: float
+    aicc: float | None
+
+
+def count_parameters(model: HmmModel) -> int:
+    """training.py:82-86."""
+    k = model.num_states
+    return (k - 1) + k * (k - 1) + sum(d.num_free_params() for d in model.emissions)
+
+
+_FAM_NAME = {v: k for k, v in _native.FAM.items()}
+
+_ERR_TEXT = {
+    _native.MS_ERR_NO_MASS: lambda fam: "fit requires positive total weight",
+    _native.MS_ERR_SUPPORT: lambda fam: {
+        "poisson": "poisson fit requires non-negative integer observations",
+        "gamma": "gamma fit requires strictly positive observations",
+    }.get(fam, f"{fam} fit support violation"),
+    _native.MS_ERR_GAMMA_VAR: lambda fam: "gamma fit is degenerate: weighted variance is zero",
+    _native.MS_ERR_GAMMA_GAP: lambda fam: "gamma fit is degenerate: zero log-moment gap",
+    _native.MS_ERR_NONFINITE: lambda fam: "von_mises fit requires finite angles",
+}
+
+
+def _warn_texts(fam: str, st: int) -> list[str]:
+    out = []
+    if fam == "gamma" and st & _native.MS_WARN_NEWTON:
+        out.append("gamma shape update did not converge; using moment seed")
+    if fam == "von_mises":
+        if st & _native.MS_WARN_BOUNDARY:
+            out.append("von_mises resultant length is at the boundary; clamping concentration")
+        if st & _native.MS_WARN_CEILING:
+            out.append("von_mises concentration clamped at ceiling")
+        if st & _native.MS_WARN_NEWTON:
+            out.append("von_mises concentration update did not converge")
+    if fam == "student_t" and st & _native.MS_WARN_CEILING:
+        out.append("student_t degrees of freedom clamped; near-Gaussian state")
+    return out
+
+
+def model_from_record(rec: np.ndarray) -> HmmModel:
+    """HmmModel from a device loghmm_model_t read back to the host."""
+    K = int(rec["K"])
+    ns = int(rec["n_streams"])
+    ems = []
+    for j in range(K):
+        parts = [from_record(int(rec["em"][s, j]["family"]), rec["em"][s, j]["p"]) for s in range(ns)]
+        ems.append(parts[0] if ns == 1 else Joint(parts[0], parts[1]))
+    pi = np.array(rec["pi"][:K], dtype=float)
+    A = np.array(rec["A"][: K * K], dtype=float).reshape(K, K)
+    return HmmModel(pi, A, tuple(ems))
+
+
+def _check_estep(flags: np.ndarray, ll: np.ndarray) -> None:
+    """Reference error order: NaN at validation, then per sequence the dead
+    observation check (training.py:189-194) and the -inf LL check (:196-197)."""
+    if (flags[:, 1] & 1).any():
+        raise ValueError("observation sequence contains NaN")
+    bad = np.nonzero((flags[:, 0] >= 0) | (ll == -np.inf))[0]
+    if bad.size:
+        s = int(bad[0])
+        if flags[s, 0] >= 0:
+            raise TrainingError(
+                "observation outside the support of every state: "
+                f"sequence {s}, index {int(flags[s, 0])}"
+            )
+        raise TrainingError(f"sequence {s} is impossible under the model")
+
+
+def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtype="float64"):
+    """EM training: returns the refined model and the per-iteration trace."""
+    config = config or TrainingConfig()
+    ns = model.n_streams
+    batch = engine.make_batch(data, ns, dtype)
+    K = model.num_states
+    dm_cur = engine.DeviceModel.from_model(model)
+    dm_next = engine.DeviceModel.empty_like(dm_cur)
+    fams = [[int(dm_cur.host["em"][s, j]["family"]) for j in range(K)] for s in range(ns)]
+    student = [(s, j) for s in range(ns) for j in range(K) if fams[s][j] == _native.FAM["student_t"]]
+    student_streams = sorted({s for s, _ in student})
+    dev = batch.y0.device
+    out = engine.forward_backward(batch, dm_cur, alpha=False, beta=False, gamma=bool(student),
+                                  stats=True)
+    totals = torch.empty(out.partials.shape[1] + 1, dtype=torch.float64, device=dev)
+    status = torch.zeros(ns * K, dtype=torch.int32, device=dev)
+    guard = torch.zeros(ns * K * 8, dtype=torch.float64, device=dev)
+    need_more = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    trace: list[float] = []
+    collapsed_states: list[tuple[int, int]] = []
+    converged = False
+    n_msteps = 0
+    for iteration in range(1, config.max_iterations + 1):
+        if iteration > 1:
+            engine.forward_backward(batch, dm_cur, alpha=False, beta=False, gamma=bool(student),
+                                    stats=True, out=out)
+        engine.reduce_stats(out.partials, out.ll, totals)
+        flags = out.flags.cpu().numpy()
+        ll = out.ll.cpu().numpy()
+        _check_estep(flags, ll)
+        total_ll = float(totals[-1].item())
+        trace.append(total_ll)
+        if len(trace) >= 2:
+            delta = trace[-1] - trace[-2]
+            if delta == 0.0 or abs(delta) < config.rel_tol * abs(trace[-1]):
+                converged = True
+                break
+        if iteration == config.max_iterations:
+            break
+        engine.mstep(dm_cur, totals, batch.B, config, dm_next, status, guard)
+        for s in student_streams:
+            ncand = 2
+            while True:
+                need_more.zero_()
+                engine.student_guard(batch, dm_next, out.gamma, s, ncand, guard, status, need_more)
+                if int(need_more.item()) == 0:
+                    break
+                ncand = _native.GUARD_CANDIDATES
+        st = status.cpu().numpy()
+        for j in range(K):
+            for s in range(ns):
+                code = int(st[s * K + j])
+                fam = _FAM_NAME[fams[s][j]]
+                base = code & 0xFF
+                if base >= 16:
+                    raise TrainingError(f"state {j}: {_ERR_TEXT[base](fam)}")
+                for msg in _warn_texts(fam, code):
+                    warnings.warn(msg, FitWarning, stacklevel=2)
+            if int(st[j]) & 0xFF == _native.MS_COLLAPSED:
+                collapsed_states.append((iteration, j))
+        dm_cur, dm_next = dm_next, dm_cur
+        n_msteps += 1
+
+    current = model if n_msteps == 0 else model_from_record(dm_cur.to_host())
+    report = TrainingReport(
+        log_likelihood_trace=trace,
+        iterations=len(trace),
+        converged=converged,
+        collapsed_states=collapsed_states,
+    )
+    return current, report
+
+
+def score_model(model: HmmModel, data, dtype="float64") -> ModelScore:
+    """Log-likelihood over all sequences plus AIC/BIC/AICc (training.py:89-102)."""
+    batch = engine.make_batch(data, model.n_streams, dtype)
+    dm = engine.DeviceModel.from_model(model)
+    o = engine.forward_backward(batch, dm, alpha=False, beta=False, gamma=False)
+    flags = o.flags.cpu().numpy()
+    if (flags[:, 1] & 1).any():
+        raise ValueError("observation sequence contains NaN")
+    total_ll = float(np.sum(o.ll.cpu().numpy()))
+    n = batch.N
+    p = count_parameters(model)
+    aic = 2.0 * p - 2.0 * total_ll
+    bic = p * math.log(n) - 2.0 * total_ll
+    aicc = aic + 2.0 * p * (p + 1.0) / (n - p - 1.0) if n > p + 1 else None
+    return ModelScore(total_ll, p, n, aic, bic, aicc)
+
+
+# ---------------------------------------------------------------------------
+# host-side initialisation (training.py:239-282; distributions.py:1114-1176)
+# ---------------------------------------------------------------------------
+def _mean_var(y: np.ndarray):
+    n = float(y.size)
+    w = np.ones_like(y)
+    mean = float(np.dot(w, y) / n)
+    var = float(np.dot(w, (y - mean) ** 2) / n)
+    return n, mean, var
+
+
+def _moment_seed(family: str, y: np.ndarray) -> Distribution:
+    n, mean, var = _mean_var(y)
+    sd = max(math.sqrt(var), SCALE_FLOOR)
+    if family == "gaussian":
+        return Gaussian(mean, sd)
+    if family == "poisson":
+        return Poisson(max(mean, SCALE_FLOOR))
+    if family == "von_mises":
+        w = np.ones_like(y)
+        s = float(np.dot(w, np.sin(y)))
+        c = float(np.dot(w, np.cos(y)))
+        mu = math.atan2(s, c)
+        if mu <= -math.pi:
+            mu = math.pi
+        rbar = min(math.hypot(s, c) / n, 1.0 - 1e-9)
+        kappa = rbar * (2.0 - rbar * rbar) / (1.0 - rbar * rbar)
+        return VonMises(mu, min(kappa, VONMISES_KAPPA_CEILING))
+    if family == "gamma":
+        if (y <= 0).any():
+            raise ValueError("gamma fit requires strictly positive observations")
+        shape = mean * mean / var if var > 0 else 1.0
+        return Gamma(max(shape, SCALE_FLOOR), max(shape, SCALE_FLOOR) / max(mean, SCALE_FLOOR))
+    if family == "student_t":
+        return StudentT(mean, sd, 10.0)
+    raise ValueError(f"unknown family '{family}'")
+
+
+def default_initial_model(num_states: int, families, data) -> HmmModel:
+    """Deterministic starting model: pooled observations sorted and split into
+    quantile bins, one per state, each seeded from its bin's moments; uniform
+    start with sticky diagonals (training.py:239-282)."""
+    if num_states < 1:
+        raise ValueError("num_states must be positive")
+    if isinstance(families, str):
+        families = [families]
+    families = list(families)
+    if len(families) == 1:
+        families = families * num_states
+    if len(families) != num_states:
+        raise ValueError(f"expected 1 or {num_states} family names, got {len(families)}")
+    if isinstance(data, np.ndarray) and data.ndim == 1:
+        data = [data]
+    seqs = [np.asarray(s, dtype=float) for s in data]
+    if not seqs:
+        raise TrainingError("training data contains no sequences")
+    pooled = np.sort(np.concatenate([s.reshape(-1) for s in seqs]))
+    bins = np.array_split(pooled, num_states)
+    emissions = []
+    for family, chunk in zip(families, bins):
+        if chunk.size == 0:
+            raise TrainingError("more states than observations; cannot seed bins")
+        emissions.append(_moment_seed(family, chunk))
+    pi = np.full(num_states, 1.0 / num_states)
+    if num_states == 1:
+        a = np.array([[1.0]])
+    else:
+        off = 0.1 / (num_states - 1)
+        a = np.full((num_states, num_states), off)
+        np.fill_diagonal(a, 0.9)
+    return HmmModel(pi, a, tuple(emissions))

@@ -1,0 +1,383 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle and
+the reference's golden vectors.
+
+Tolerances (BASELINE.json north_star):
+  fp64: LL / params <= 1e-9 relative, posteriors <= 1e-9 absolute
+  fp32: LL <= 1e-4 relative, posteriors <= 1e-5 absolute
+  Viterbi paths / backpointers: bit-exact (fp64 vs the reference for the
+  IEEE-basic-op families Gaussian and Poisson; fp32 vs the fp32 restatement);
+  for Student-t / Gamma / von Mises the emission calls log1p/log/cos whose
+  last ulp differs between CUDA and numpy, so a differing backpointer is only
+  accepted at a near-tie (candidate gap within 64 ulps of the score).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import loghmm_oracle as O  # noqa: E402
+
+import paper_2605_29208_b200 as H  # noqa: E402
+from paper_2605_29208_b200 import engine  # noqa: E402
+from paper_2605_29208_b200.configs import make_config  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def to_model(pi, A, ems):
+    d = []
+    for e in ems:
+        k = e[0]
+        if k == "gaussian":
+            d.append(H.Gaussian(e[1], e[2]))
+        elif k == "student_t":
+            d.append(H.StudentT(e[1], e[2], e[3]))
+        elif k == "gamma":
+            d.append(H.Gamma(e[1], e[2]))
+        elif k == "von_mises":
+            d.append(H.VonMises(e[1], e[2]))
+        elif k == "poisson":
+            d.append(H.Poisson(e[1]))
+        elif k == "joint":
+            d.append(H.Joint(to_model([1.0], [[1.0]], [e[1]]).emissions[0],
+                             to_model([1.0], [[1.0]], [e[2]]).emissions[0]))
+    return H.HmmModel(pi, A, tuple(d))
+
+
+def to_tuples(model):
+    out = []
+    for d in model.emissions:
+        if isinstance(d, H.Joint):
+            out.append(("joint", to_tuples(H.HmmModel([1.0], [[1.0]], (d.first,)))[0],
+                        to_tuples(H.HmmModel([1.0], [[1.0]], (d.second,)))[0]))
+        else:
+            out.append((d.family,) + tuple(d.params().values()))
+    return out
+
+
+EXACT_FAMS = ("gaussian", "poisson")
+
+
+def test_emission_matches_reference(golden):
+    for c in golden["cases"]:
+        m = to_model(c["pi"], c["A"], c["emissions"])
+        y = golden["vec"][c["name"] + "_y"]
+        lb = H.emission_log_matrix(m, y)
+        ref = golden["vec"][c["name"] + "_logb"]
+        if c["family"] in EXACT_FAMS:
+            assert np.array_equal(lb, ref), c["name"]
+        else:
+            np.testing.assert_allclose(lb, ref, rtol=1e-13, atol=1e-13, err_msg=c["name"])
+
+
+def test_posteriors_match_reference(golden):
+    v = golden["vec"]
+    for c in golden["cases"]:
+        m = to_model(c["pi"], c["A"], c["emissions"])
+        y = v[c["name"] + "_y"]
+        fb = H.posteriors(m, y, include_xi=True)
+        assert fb.log_likelihood == pytest.approx(c["ll"], rel=1e-9), c["name"]
+        np.testing.assert_allclose(fb.gamma, v[c["name"] + "_gamma"], atol=1e-9, err_msg=c["name"])
+        np.testing.assert_allclose(fb.log_alpha, v[c["name"] + "_log_alpha"], rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(fb.log_beta, v[c["name"] + "_log_beta"], rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(fb.xi, v[c["name"] + "_xi"], atol=1e-9, err_msg=c["name"])
+        np.testing.assert_allclose(fb.gamma.sum(axis=1), 1.0, atol=1e-12)
+
+
+def _near_tie_ok(lp, la, lb, t, j, ours, theirs, dtype=np.float64):
+    """Backpointer disagreement is allowed only at a near-tie of the two
+    candidates (|gap| within 64 ulps of the score magnitude)."""
+    # recompute the oracle's score at t-1 in the same precision
+    R = dtype
+    score = np.asarray(lp, R) + np.asarray(lb[0], R)
+    for s in range(1, t):
+        cand = score[:, None] + np.asarray(la, R)
+        score = cand[np.argmax(cand, axis=0), np.arange(len(score))] + np.asarray(lb[s], R)
+    cand = score[:, None] + np.asarray(la, R)
+    gap = abs(float(cand[ours, j]) - float(cand[theirs, j]))
+    return gap <= 64 * np.finfo(R).eps * max(1.0, abs(float(cand[theirs, j])))
+
+
+def test_viterbi_matches_reference(golden):
+    v = golden["vec"]
+    for c in golden["cases"]:
+        m = to_model(c["pi"], c["A"], c["emissions"])
+        y = v[c["name"] + "_y"]
+        res = H.viterbi(m, y)
+        bv = H.viterbi_batch(m, y, back=True)
+        back = bv.back.cpu().numpy().astype(np.int64)
+        lp, la = O.model_tables(c["pi"], c["A"])
+        lbm = v[c["name"] + "_logb"]
+        opath, olj, oback = O.viterbi(lp, la, lbm)
+        if c["family"] in EXACT_FAMS:
+            assert np.array_equal(res.path, v[c["name"] + "_path"]), c["name"]
+            assert res.log_joint == c["log_joint"], c["name"]
+            assert np.array_equal(back, oback), c["name"]
+        else:
+            diff = np.argwhere(back != oback)
+            for t, j in diff:
+                assert _near_tie_ok(lp, la, lbm, t, j, back[t, j], oback[t, j]), (c["name"], t, j)
+            if diff.size == 0:
+                assert np.array_equal(res.path, v[c["name"] + "_path"])
+            assert res.log_joint == pytest.approx(c["log_joint"], rel=1e-12)
+
+
+def _random_gauss_model(rng, K):
+    pi = rng.dirichlet(np.ones(K))
+    A = rng.dirichlet(np.ones(K), size=K) * 0.4 + 0.6 * np.eye(K)
+    A /= A.sum(1, keepdims=True)
+    return H.HmmModel(pi, A, tuple(H.Gaussian(float(rng.normal(0, 2)), float(rng.uniform(0.4, 1.5)))
+                                   for _ in range(K)))
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5, 8])
+def test_fp32_viterbi_bitexact_ragged(K):
+    rng = np.random.default_rng(100 + K)
+    m = _random_gauss_model(rng, K)
+    lens = [1, 2, 31, 32, 33, 64, 100, 257, 1024, 700]
+    seqs = [rng.normal(0, 3, n) for n in lens]
+    out = H.viterbi_batch(m, seqs, dtype="float32", back=True)
+    path = out.path.cpu().numpy()
+    back = out.back.cpu().numpy()
+    lj = out.log_joint.cpu().numpy()
+    lp, la = O.model_tables(m.initial, m.transitions)
+    off = out.offsets
+    for b, y in enumerate(seqs):
+        lb32 = O.emission_matrix(to_tuples(m), y.astype(np.float32), np.float32)
+        p, j, bk = O.viterbi(lp.astype(np.float32), la.astype(np.float32), lb32, np.float32)
+        assert np.array_equal(path[off[b]:off[b + 1]], p), (K, b)
+        assert np.array_equal(back[off[b]:off[b + 1]], bk), (K, b)
+        assert lj[b] == j
+
+
+@pytest.mark.parametrize("K", [2, 4, 7])
+def test_fp64_viterbi_poisson_bitexact(K):
+    rng = np.random.default_rng(7 + K)
+    pi = rng.dirichlet(np.ones(K))
+    A = rng.dirichlet(np.ones(K), size=K)
+    m = H.HmmModel(pi, A, tuple(H.Poisson(float(r)) for r in rng.uniform(0.5, 20, K)))
+    seqs = [rng.poisson(8.0, n).astype(float) for n in (5, 77, 300, 1500)]
+    out = H.viterbi_batch(m, seqs, back=True)
+    lp, la = O.model_tables(pi, A)
+    for b, y in enumerate(seqs):
+        p, j, bk = O.viterbi(lp, la, O.emission_matrix(to_tuples(m), y))
+        s = slice(out.offsets[b], out.offsets[b + 1])
+        assert np.array_equal(out.path.cpu().numpy()[s], p)
+        assert np.array_equal(out.back.cpu().numpy()[s].astype(np.int64), bk)
+        assert out.log_joint.cpu().numpy()[b] == j
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 6, 8])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_posteriors_batch_ragged(K, dtype):
+    rng = np.random.default_rng(11 * K)
+    m = _random_gauss_model(rng, K)
+    lens = [1, 2, 5, 31, 32, 33, 100, 1000, 1025]
+    seqs = [rng.normal(0, 3, n) for n in lens]
+    r = H.posteriors_batch(m, seqs, dtype=dtype, include_xi=True)
+    lp, la = O.model_tables(m.initial, m.transitions)
+    g = r.gamma.cpu().numpy().astype(np.float64)
+    A_ = r.log_alpha.cpu().numpy().astype(np.float64)
+    B_ = r.log_beta.cpu().numpy().astype(np.float64)
+    X_ = r.xi.cpu().numpy().astype(np.float64)
+    ll = r.log_likelihood.cpu().numpy()
+    for b, y in enumerate(seqs):
+        yy = y.astype(np.float32).astype(np.float64) if dtype == "float32" else y
+        o = O.posteriors(lp, la, O.emission_matrix(to_tuples(m), yy), include_xi=True)
+        s = slice(r.offsets[b], r.offsets[b + 1])
+        xs = slice(r.offsets[b] - b, r.offsets[b + 1] - b - 1)
+        if dtype == "float64":
+            assert ll[b] == pytest.approx(o["ll"], rel=1e-9)
+            np.testing.assert_allclose(g[s], o["gamma"], atol=1e-9)
+            np.testing.assert_allclose(A_[s], o["log_alpha"], rtol=1e-9, atol=1e-9)
+            np.testing.assert_allclose(B_[s], o["log_beta"], rtol=1e-9, atol=1e-9)
+            np.testing.assert_allclose(X_[xs], o["xi"], atol=1e-9)
+        else:
+            assert ll[b] == pytest.approx(o["ll"], rel=1e-4)
+            np.testing.assert_allclose(g[s], o["gamma"], atol=1e-5)
+            np.testing.assert_allclose(A_[s], o["log_alpha"], rtol=1e-5, atol=1e-3)
+            np.testing.assert_allclose(B_[s], o["log_beta"], rtol=1e-5, atol=1e-3)
+            np.testing.assert_allclose(X_[xs], o["xi"], atol=1e-5)
+
+
+def test_baum_welch_matches_reference(golden):
+    v = golden["vec"]
+    for c in golden["cases"]:
+        m = to_model(c["pi"], c["A"], c["emissions"])
+        y = v[c["name"] + "_y"]
+        cfg = H.TrainingConfig(max_iterations=c["bw"]["max_iterations"], rel_tol=1e-300)
+        fitted, rep = H.baum_welch(m, [y, y[::-1].copy()], cfg)
+        np.testing.assert_allclose(rep.log_likelihood_trace, c["bw"]["trace"], rtol=1e-9, err_msg=c["name"])
+        np.testing.assert_allclose(fitted.initial, v[c["name"] + "_bw_pi"], atol=1e-9)
+        np.testing.assert_allclose(fitted.transitions, v[c["name"] + "_bw_A"], atol=1e-9)
+        for a, b in zip(to_tuples(fitted), c["bw"]["emissions"]):
+            assert a[0] == b[0]
+            np.testing.assert_allclose(a[1:], b[1:], rtol=1e-8, err_msg=c["name"])
+        assert [list(x) for x in rep.collapsed_states] == c["bw"]["collapsed"]
+
+
+def test_config1(golden):
+    v, c1 = golden["vec"], golden["c1"]
+    cfg = make_config("c1")
+    y = cfg.data[0]
+    assert np.array_equal(y, v["c1_y"])
+    fb = H.posteriors(cfg.init, y)
+    assert fb.log_likelihood == pytest.approx(c1["ll"], rel=1e-12)
+    np.testing.assert_allclose(fb.gamma, v["c1_gamma"], atol=1e-10)
+    vit = H.viterbi(cfg.init, y)
+    assert np.array_equal(vit.path, v["c1_path"]) and vit.log_joint == c1["log_joint"]
+    fitted, rep = H.baum_welch(cfg.init, [y], H.TrainingConfig(max_iterations=2, rel_tol=1e-300))
+    np.testing.assert_allclose(rep.log_likelihood_trace, c1["bw_trace"], rtol=1e-12)
+    np.testing.assert_allclose(fitted.transitions, c1["bw_A"], atol=1e-10)
+    for a, b in zip(to_tuples(fitted), c1["bw_emissions"]):
+        np.testing.assert_allclose(a[1:], b[1:], rtol=1e-9)
+
+
+def test_earthquake_fixture(golden):
+    eq = golden["front"]["earthquake"]
+    y = np.array(eq["observations"], dtype=float)
+    exp = eq["expected"]
+    start = H.default_initial_model(2, "poisson", [y])
+    fitted, rep = H.baum_welch(start, [y])
+    assert rep.converged and rep.iterations == exp["iterations"]
+    assert rep.log_likelihood_trace[-1] == pytest.approx(exp["log_likelihood"], abs=1e-9)
+    assert sorted(d.rate for d in fitted.emissions) == pytest.approx(exp["rates_sorted"], rel=1e-9)
+    assert H.viterbi(fitted, y).path.tolist() == exp["viterbi_path"]
+    assert H.posterior_decode(H.posteriors(fitted, y)).tolist() == exp["posterior_path"]
+    sc = H.score_model(fitted, [y])
+    assert sc.log_likelihood == pytest.approx(exp["score"]["log_likelihood"], abs=1e-9)
+    assert sc.num_params == exp["score"]["num_params"]
+
+
+def test_small_model_fixtures(golden):
+    for case in golden["front"]["small_models"]:
+        doc = case["model_document"]
+        m = to_model(doc["initial"], doc["transitions"],
+                     [("gaussian", e["params"]["mu"], e["params"]["sigma"]) for e in doc["emissions"]])
+        y = np.array(case["observations"], dtype=float)
+        fb = H.posteriors(m, y)
+        assert fb.log_likelihood == pytest.approx(case["expected"]["log_likelihood"], abs=1e-12)
+        assert H.viterbi(m, y).path.tolist() == case["expected"]["viterbi_path"]
+        assert H.posterior_decode(fb).tolist() == case["expected"]["posterior_path"]
+
+
+def test_underflow_100k(golden):
+    u = golden["underflow"]
+    rng = np.random.default_rng(7)
+    m = H.HmmModel([0.5, 0.5], [[0.97, 0.03], [0.05, 0.95]], (H.Gaussian(0.0, 1.0), H.Gaussian(2.5, 1.8)))
+    seq = rng.normal(size=100_000) * 2.0 + 1.0
+    fb = H.posteriors(m, seq)
+    assert fb.log_likelihood == pytest.approx(u["ll"], rel=1e-9)
+    np.testing.assert_allclose(fb.gamma[0], u["gamma_row0"], atol=1e-9)
+    np.testing.assert_allclose(fb.gamma[-1], u["gamma_last"], atol=1e-9)
+    assert np.abs(fb.gamma.sum(axis=1) - 1.0).max() < 1e-6
+    assert H.viterbi(m, seq).log_joint == u["viterbi_log_joint"]
+    fb32 = H.posteriors(m, seq, dtype="float32")
+    assert fb32.log_likelihood == pytest.approx(u["ll"], rel=1e-4)
+
+
+def test_error_semantics():
+    m = H.HmmModel([0.5, 0.5], [[0.5, 0.5], [0.5, 0.5]], (H.Poisson(2.0), H.Poisson(5.0)))
+    with pytest.raises(H.InfeasibleSequenceError, match="sequence impossible under model"):
+        H.posteriors(m, np.array([1.0, 2.5, 3.0]))
+    with pytest.raises(H.InfeasibleSequenceError, match="no feasible path"):
+        H.viterbi(m, np.array([1.0, 2.5, 3.0]))
+    with pytest.raises(H.TrainingError, match="sequence 1, index 2"):
+        H.baum_welch(m, [np.array([1.0, 2.0]), np.array([1.0, 2.0, 0.5])],
+                     H.TrainingConfig(max_iterations=2))
+    with pytest.raises(ValueError, match="NaN"):
+        H.posteriors(m, np.array([1.0, np.nan]))
+    with pytest.raises(ValueError, match="non-empty"):
+        H.posteriors(m, np.array([]))
+
+
+def test_single_state_and_single_step():
+    m = H.HmmModel([1.0], [[1.0]], (H.Gaussian(0.3, 1.7),))
+    y = np.array([0.1, -2.0, 3.3])
+    fb = H.posteriors(m, y)
+    assert fb.log_likelihood == pytest.approx(float(O.emission_matrix([("gaussian", 0.3, 1.7)], y).sum()), rel=1e-12)
+    m2 = _random_gauss_model(np.random.default_rng(1), 3)
+    fb1 = H.posteriors(m2, np.array([0.4]))
+    lp, la = O.model_tables(m2.initial, m2.transitions)
+    o = O.posteriors(lp, la, O.emission_matrix(to_tuples(m2), np.array([0.4])))
+    assert fb1.log_likelihood == pytest.approx(o["ll"], rel=1e-12)
+    assert np.array_equal(fb1.log_beta, np.zeros((1, 3)))
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_config2_full_size(dtype):
+    """BASELINE config 2 at full size (B=4096, T=1024): size-independent
+    properties on all sequences, oracle parity on a seeded subset."""
+    cfg = make_config("c2")
+    model = cfg.init
+    r = H.posteriors_batch(model, cfg.data, dtype=dtype)
+    vit = H.viterbi_batch(model, cfg.data, dtype=dtype)
+    g = r.gamma.double()
+    assert torch.isfinite(r.log_likelihood).all()
+    assert (g.sum(dim=1) - 1).abs().max().item() < (1e-12 if dtype == "float64" else 1e-5)
+    assert (vit.log_joint <= r.log_likelihood + 1e-6 * r.log_likelihood.abs()).all()
+    rng = np.random.default_rng(5)
+    lp, la = O.model_tables(model.initial, model.transitions)
+    T = cfg.T
+    for b in rng.choice(cfg.B, 6, replace=False):
+        y = cfg.data[b]
+        yy = y.astype(np.float32).astype(np.float64) if dtype == "float32" else y
+        o = O.posteriors(lp, la, O.emission_matrix(to_tuples(model), yy))
+        s = slice(b * T, (b + 1) * T)
+        tol_ll, tol_g = (1e-9, 1e-9) if dtype == "float64" else (1e-4, 1e-5)
+        assert r.log_likelihood[b].item() == pytest.approx(o["ll"], rel=tol_ll)
+        np.testing.assert_allclose(r.gamma[s].double().cpu().numpy(), o["gamma"], atol=tol_g)
+        if dtype == "float64":
+            p, j, _ = O.viterbi(lp, la, O.emission_matrix(to_tuples(model), y))
+        else:
+            p, j, _ = O.viterbi(lp.astype(np.float32), la.astype(np.float32),
+                                O.emission_matrix(to_tuples(model), y.astype(np.float32), np.float32),
+                                np.float32)
+        assert np.array_equal(vit.path[s].cpu().numpy(), p)
+        assert vit.log_joint[b].item() == j
+
+
+@pytest.mark.parametrize("name,B,T,iters", [("c2", 48, 1024, 3), ("c3", 16, 2048, 3),
+                                            ("c4", 12, 2000, 3), ("c5", 2, 4096, 2)])
+def test_config_baum_welch_subset(name, B, T, iters):
+    """Baum-Welch parity on a seeded subset of each BASELINE config."""
+    cfg = make_config(name, B=B, T=T)
+    data = [cfg.data[b] for b in range(B)]
+    fitted, rep = H.baum_welch(cfg.init, data, H.TrainingConfig(max_iterations=iters, rel_tol=1e-300))
+    pi, A, em, trace, _, _ = O.baum_welch(cfg.init.initial, cfg.init.transitions, to_tuples(cfg.init),
+                                          data, iters)
+    np.testing.assert_allclose(rep.log_likelihood_trace, trace, rtol=1e-9)
+    np.testing.assert_allclose(fitted.transitions, A, atol=1e-9)
+    np.testing.assert_allclose(fitted.initial, pi, atol=1e-9)
+    for a, b in zip(to_tuples(fitted), em):
+        if a[0] == "joint":
+            np.testing.assert_allclose(a[1][1:], b[1][1:], rtol=1e-8)
+            np.testing.assert_allclose(a[2][1:], b[2][1:], rtol=1e-8)
+        else:
+            np.testing.assert_allclose(a[1:], b[1:], rtol=1e-8)
+
+
+def test_config5_viterbi_and_posteriors_subset():
+    cfg = make_config("c5", B=2, T=3000)
+    model = cfg.truth
+    lp, la = O.model_tables(model.initial, model.transitions)
+    r = H.posteriors_batch(model, cfg.data)
+    vit = H.viterbi_batch(model, cfg.data, back=True)
+    for b in range(2):
+        lb = O.emission_matrix(to_tuples(model), cfg.data[b])
+        o = O.posteriors(lp, la, lb)
+        s = slice(b * cfg.T, (b + 1) * cfg.T)
+        assert r.log_likelihood[b].item() == pytest.approx(o["ll"], rel=1e-9)
+        np.testing.assert_allclose(r.gamma[s].cpu().numpy(), o["gamma"], atol=1e-9)
+        p, j, bk = O.viterbi(lp, la, lb)
+        assert np.array_equal(vit.path[s].cpu().numpy(), p)
+        assert np.array_equal(vit.back[s].cpu().numpy().astype(np.int64), bk)
+        assert vit.log_joint[b].item() == j
