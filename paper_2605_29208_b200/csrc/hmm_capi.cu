@@ -71,7 +71,9 @@ static FBGeom fb_geom(int K, int esz, int n_streams, int64_t max_T) {
   int L = (int)((max_T + kWarp - 1) / kWarp);
   if (L < 1) L = 1;
   g.Lmax = ((L + g.L_align - 1) / g.L_align) * g.L_align;
-  g.y_pitch = g.Lmax | 1;  // odd pitch: lane rows fall in distinct banks
+  // y: contiguous [32*Lmax] with one pad element per 32 (t + t/32), per lane row of
+  // the carve = y_pitch elements so that 32*y_pitch covers it
+  g.y_pitch = g.Lmax + (g.Lmax + 31) / 32 + 1;
   const int V = (kb % 16 == 0) ? 16 : (kb % 8 == 0) ? 8 : 4;
   int aunits = g.Lmax * kb / V;
   if ((aunits & 1) == 0) aunits += 1;
@@ -126,17 +128,17 @@ static cudaError_t dispatch_fb_small(int K, const FBArgs& a, int cfg, bool gl, d
 }
 
 template <typename R>
-static cudaError_t dispatch_vit_small(int K, const VitArgs& a, bool gl, dim3 grid, dim3 block,
-                                      size_t smem, cudaStream_t st) {
+static cudaError_t dispatch_vit_small(int K, const VitArgs& a, int cfg, bool gl, dim3 grid,
+                                      dim3 block, size_t smem, cudaStream_t st) {
   switch (K) {
-    case 1: return launch_vit_small<R, 1>(a, gl, grid, block, smem, st);
-    case 2: return launch_vit_small<R, 2>(a, gl, grid, block, smem, st);
-    case 3: return launch_vit_small<R, 3>(a, gl, grid, block, smem, st);
-    case 4: return launch_vit_small<R, 4>(a, gl, grid, block, smem, st);
-    case 5: return launch_vit_small<R, 5>(a, gl, grid, block, smem, st);
-    case 6: return launch_vit_small<R, 6>(a, gl, grid, block, smem, st);
-    case 7: return launch_vit_small<R, 7>(a, gl, grid, block, smem, st);
-    default: return launch_vit_small<R, 8>(a, gl, grid, block, smem, st);
+    case 1: return launch_vit_small<R, 1>(a, cfg, gl, grid, block, smem, st);
+    case 2: return launch_vit_small<R, 2>(a, cfg, gl, grid, block, smem, st);
+    case 3: return launch_vit_small<R, 3>(a, cfg, gl, grid, block, smem, st);
+    case 4: return launch_vit_small<R, 4>(a, cfg, gl, grid, block, smem, st);
+    case 5: return launch_vit_small<R, 5>(a, cfg, gl, grid, block, smem, st);
+    case 6: return launch_vit_small<R, 6>(a, cfg, gl, grid, block, smem, st);
+    case 7: return launch_vit_small<R, 7>(a, cfg, gl, grid, block, smem, st);
+    default: return launch_vit_small<R, 8>(a, cfg, gl, grid, block, smem, st);
   }
 }
 
@@ -295,8 +297,10 @@ int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm
     const int64_t G = kWarp / K;
     const int64_t warps = (B + G - 1) / G;
     dim3 grid((unsigned)((warps + g.wpb - 1) / g.wpb)), block(32 * g.wpb);
-    e = dtype == LOGHMM_F64 ? dispatch_vit_small<double>(K, a, g.global, grid, block, g.smem, st)
-                            : dispatch_vit_small<float>(K, a, g.global, grid, block, g.smem, st);
+    int fams = 0;
+    const int cfg = cfg_of(h_desc, &fams);
+    e = dtype == LOGHMM_F64 ? dispatch_vit_small<double>(K, a, cfg, g.global, grid, block, g.smem, st)
+                            : dispatch_vit_small<float>(K, a, cfg, g.global, grid, block, g.smem, st);
   } else {
     const int esz = dtype == LOGHMM_F64 ? 8 : 4;
     const int threads = 32 * ((K + 31) / 32);

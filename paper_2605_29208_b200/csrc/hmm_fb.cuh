@@ -110,36 +110,58 @@ struct VecIO {
 };
 
 // Write the staged rows of a slab window to global memory.  Row c (lane c's
-// chunk) covers global steps t0_c + sb + [0, n_c); its bytes are contiguous
-// in the [N, K] output, so lanes cooperatively copy 16-byte units row by row.
+// chunk) covers global steps c*L + sb + [0, n_c); its bytes are contiguous in
+// the [N, K] output, so the 32 lanes copy 16-byte units row by row.  The row
+// geometry is fixed per sequence and precomputed once (FlushPlan).
+template <typename R, int K>
+struct FlushPlan {
+  static constexpr int ROW = kSlab * K;                 // elements per full row
+  static constexpr int EPV = 16 / (int)sizeof(R);       // elements per 16 B
+  static constexpr int VPR = (ROW + EPV - 1) / EPV;     // 16 B units per row
+  static constexpr int NIT = (kWarp * VPR + kWarp - 1) / kWarp;
+  int64_t gbase[NIT];  // element offset of (row start, unit) in the output
+  int soff[NIT];       // element offset in the stage buffer
+  int clen[NIT];       // chunk length of the row (steps)
+  int e0[NIT];         // element offset of the unit inside the row
+  bool vec_ok;
+  __device__ __forceinline__ void init(int lane, int64_t start, int L, int T, int s_pitch, bool vok) {
+    vec_ok = vok;
+#pragma unroll
+    for (int k = 0; k < NIT; ++k) {
+      const int v = lane + kWarp * k;
+      const int c = v / VPR, vi = v % VPR;
+      e0[k] = vi * EPV;
+      int cl = T - c * L;
+      cl = cl < 0 ? 0 : (cl > L ? L : cl);
+      clen[k] = c < kWarp ? cl : 0;
+      gbase[k] = (start + (int64_t)c * L) * K + e0[k];
+      soff[k] = c * s_pitch + e0[k];
+    }
+  }
+};
+
 template <typename R, int K>
 __device__ __forceinline__ void flush_slab(R* __restrict__ out, const R* __restrict__ stage,
-                                           int s_pitch, int64_t start, int L, int T, int sb,
-                                           int lane, bool vec_ok) {
-  constexpr int ROW = kSlab * K;  // elements per full row
-  if (vec_ok) {
-    constexpr int EPV = 16 / (int)sizeof(R);
-    constexpr int VPR = (ROW + EPV - 1) / EPV;  // vectors per row (ROW*sizeof(R) % 16 == 0)
-#pragma unroll 1
-    for (int v = lane; v < kWarp * VPR; v += kWarp) {
-      const int c = v / VPR, vi = v % VPR;
-      const int t0 = c * L + sb;
-      int n = T - t0;
-      n = n < 0 ? 0 : (n > kSlab ? kSlab : n);
-      const int ccap = (c + 1) * L - t0;  // steps left in this chunk from sb
-      if (n > ccap) n = ccap;
-      const int nel = n * K;
-      const int e0 = vi * EPV;
-      if (e0 >= nel) continue;
-      R* dst = out + (start + t0) * K + e0;
-      const R* src = stage + c * s_pitch + e0;
-      if (e0 + EPV <= nel) {
+                                           const FlushPlan<R, K>& fp, int s_pitch, int64_t start,
+                                           int L, int T, int sb, int lane) {
+  typedef FlushPlan<R, K> P;
+  if (fp.vec_ok) {
+#pragma unroll
+    for (int k = 0; k < P::NIT; ++k) {
+      int n = fp.clen[k] - sb;
+      n = n > kSlab ? kSlab : n;
+      const int nel = n * K - fp.e0[k];
+      if (nel <= 0) continue;
+      R* dst = out + fp.gbase[k] + (int64_t)sb * K;
+      const R* src = stage + fp.soff[k];
+      if (nel >= P::EPV) {
         *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
       } else {
-        for (int e = 0; e < nel - e0; ++e) dst[e] = src[e];
+        for (int e = 0; e < nel; ++e) dst[e] = src[e];
       }
     }
   } else {
+    constexpr int ROW = P::ROW;
 #pragma unroll 1
     for (int v = lane; v < kWarp * ROW; v += kWarp) {
       const int c = v / ROW, e = v % ROW;
@@ -432,25 +454,38 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
     nn = lg <= 0.0 ? 8 : (int)fmin(8.0, fmax(1.0, floor(budget / lg)));
   }
 
-  // ---- stage y into shared memory (coalesced), chunk-major with odd pitch --
+  // ---- stage y into shared memory: coalesced batched loads (8 in flight per
+  // lane), stored contiguously with one pad element every 32 so lane-strided
+  // chunk reads (stride L) hit distinct banks.
   if (!kGlobal) {
+    constexpr int UB = 8;
 #pragma unroll 1
-    for (int c = 0; c < kWarp; ++c) {
-      const int base = c * L;
-#pragma unroll 1
-      for (int s = lane; s < L; s += kWarp) {
-        const int t = base + s;
+    for (int base = 0; base < T; base += kWarp * UB) {
+      R v0[UB], v1[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int t = base + u * kWarp + lane;
+        v0[u] = t < T ? y0g[t] : R(0);
+        v1[u] = (two && t < T) ? y1g[t] : R(0);
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int t = base + u * kWarp + lane;
         if (t < T) {
-          ybuf0[c * a.y_pitch + s] = y0g[t];
-          if (two) ybuf1[c * a.y_pitch + s] = y1g[t];
+          ybuf0[t + (t >> 5)] = v0[u];
+          if (two) ybuf1[t + (t >> 5)] = v1[u];
         }
       }
     }
     __syncwarp();
   }
-  auto yat0 = [&](int s) -> R { return kGlobal ? y0g[t0 + s] : ybuf0[lane * a.y_pitch + s]; };
+  auto yat0 = [&](int s) -> R {
+    const int t = t0 + s;
+    return kGlobal ? y0g[t] : ybuf0[t + (t >> 5)];
+  };
   auto yat1 = [&](int s) -> R {
-    return two ? (kGlobal ? y1g[t0 + s] : ybuf1[lane * a.y_pitch + s]) : R(0);
+    const int t = t0 + s;
+    return two ? (kGlobal ? y1g[t] : ybuf1[t + (t >> 5)]) : R(0);
   };
 
   bool oob = false;
@@ -639,6 +674,8 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
   R* aw = kGlobal ? reinterpret_cast<R*>(a.alpha_ws) + (start + t0) * K : abuf + lane * a.a_pitch;
   const bool vec_ok = ((start * K * (int64_t)sizeof(R)) % 16 == 0) &&
                       ((L * K * (int)sizeof(R)) % 16 == 0);
+  FlushPlan<R, K> fplan;
+  fplan.init(lane, start, L, T, a.s_pitch, vec_ok);
 
   // ---- phase 3a: forward re-sweep -----------------------------------------
   R* __restrict__ outA = reinterpret_cast<R*>(a.log_alpha);
@@ -689,7 +726,7 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
       }
       if (outA && ((s % kSlab) == kSlab - 1 || s == L - 1)) {
         __syncwarp();
-        flush_slab<R, K>(outA, stA, a.s_pitch, start, L, T, s - (s % kSlab), lane, vec_ok);
+        flush_slab<R, K>(outA, stA, fplan, a.s_pitch, start, L, T, s - (s % kSlab), lane);
         __syncwarp();
       }
     }
@@ -740,7 +777,7 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
           g[j] = av[j] * q[j];
           Z += g[j];
         }
-        const R iz = R(1) / Z;
+        const R iz = N::frcp(Z);
 #pragma unroll
         for (int j = 0; j < K; ++j) g[j] *= iz;
         if (outB) {
@@ -791,7 +828,7 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
         R Z = R(0);
 #pragma unroll
         for (int i = 0; i < K; ++i) Z = fma(ap[i], q[i], Z);
-        const R iz = R(1) / Z;
+        const R iz = N::frcp(Z);
         R ai[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) ai[i] = ap[i] * iz;
@@ -841,8 +878,8 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
       }
       if (s >= 0 && (s % kSlab) == 0 && (outB || outG)) {
         __syncwarp();
-        if (outB) flush_slab<R, K>(outB, stA, a.s_pitch, start, L, T, s, lane, vec_ok);
-        if (outG) flush_slab<R, K>(outG, stB, a.s_pitch, start, L, T, s, lane, vec_ok);
+        if (outB) flush_slab<R, K>(outB, stA, fplan, a.s_pitch, start, L, T, s, lane);
+        if (outG) flush_slab<R, K>(outG, stB, fplan, a.s_pitch, start, L, T, s, lane);
         __syncwarp();
       }
     }

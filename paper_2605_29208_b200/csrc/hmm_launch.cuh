@@ -38,33 +38,47 @@ cudaError_t launch_fb_small(const FBArgs& a, int cfg, bool global, dim3 grid, di
                 : launch_fb_cfg<R, K, false>(a, cfg, grid, block, smem, st);
 }
 
-template <typename R, int K>
-cudaError_t launch_vit_small(const VitArgs& a, bool global, dim3 grid, dim3 block, size_t smem,
-                             cudaStream_t st) {
-  if (global) {
-    auto fn = viterbi_small_kernel<R, K, true>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    fn<<<grid, block, smem, st>>>(a);
-  } else {
-    auto fn = viterbi_small_kernel<R, K, false>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    fn<<<grid, block, smem, st>>>(a);
-  }
+template <typename R, int K, int CFG, bool G>
+static cudaError_t launch_vit_one(const VitArgs& a, dim3 grid, dim3 block, size_t smem,
+                                  cudaStream_t st) {
+  auto fn = viterbi_small_kernel<R, K, CFG, G>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<grid, block, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+template <typename R, int K, bool G>
+static cudaError_t launch_vit_cfg(const VitArgs& a, int cfg, dim3 grid, dim3 block, size_t smem,
+                                  cudaStream_t st) {
+  switch (cfg) {
+    case kCfgGauss: return launch_vit_one<R, K, kCfgGauss, G>(a, grid, block, smem, st);
+    case kCfgStudent: return launch_vit_one<R, K, kCfgStudent, G>(a, grid, block, smem, st);
+    case kCfgGamma: return launch_vit_one<R, K, kCfgGamma, G>(a, grid, block, smem, st);
+    case kCfgVonMises: return launch_vit_one<R, K, kCfgVonMises, G>(a, grid, block, smem, st);
+    case kCfgPoisson: return launch_vit_one<R, K, kCfgPoisson, G>(a, grid, block, smem, st);
+    case kCfgGammaVM: return launch_vit_one<R, K, kCfgGammaVM, G>(a, grid, block, smem, st);
+    default: return launch_vit_one<R, K, kCfgMixed, G>(a, grid, block, smem, st);
+  }
+}
+
+template <typename R, int K>
+cudaError_t launch_vit_small(const VitArgs& a, int cfg, bool global, dim3 grid, dim3 block,
+                             size_t smem, cudaStream_t st) {
+  return global ? launch_vit_cfg<R, K, true>(a, cfg, grid, block, smem, st)
+                : launch_vit_cfg<R, K, false>(a, cfg, grid, block, smem, st);
 }
 
 #define LHMM_DECLARE_INST(R, K)                                                              \
   template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \
                                              cudaStream_t);                                  \
-  template cudaError_t launch_vit_small<R, K>(const VitArgs&, bool, dim3, dim3, size_t,      \
+  template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
                                               cudaStream_t);
 
 #define LHMM_EXTERN_INST(R, K)                                                                      \
   extern template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \
                                                     cudaStream_t);                                  \
-  extern template cudaError_t launch_vit_small<R, K>(const VitArgs&, bool, dim3, dim3, size_t,      \
+  extern template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
                                                      cudaStream_t);
 
 }  // namespace lhmm

@@ -83,9 +83,23 @@ __device__ __forceinline__ unsigned plane_lookup(const unsigned (&pl)[NP > 0 ? N
   return r;
 }
 
-template <typename R, int K, bool kGlobal>
+template <int CFG>
+struct VitFams {
+  static constexpr int F0 = CFG == kCfgGauss     ? LOGHMM_FAM_GAUSSIAN
+                            : CFG == kCfgStudent  ? LOGHMM_FAM_STUDENT_T
+                            : CFG == kCfgGamma    ? LOGHMM_FAM_GAMMA
+                            : CFG == kCfgVonMises ? LOGHMM_FAM_VON_MISES
+                            : CFG == kCfgPoisson  ? LOGHMM_FAM_POISSON
+                            : CFG == kCfgGammaVM  ? LOGHMM_FAM_GAMMA
+                                                  : -1;
+  static constexpr int F1 = CFG == kCfgGammaVM ? LOGHMM_FAM_VON_MISES : -1;
+  static constexpr bool TWO = CFG == kCfgGammaVM || CFG == kCfgMixed;
+};
+
+template <typename R, int K, int CFG, bool kGlobal>
 __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
   typedef Num<R> N;
+  typedef VitFams<CFG> VF;
   constexpr int G = kWarp / K;
   constexpr int NP = Bits<K>::NP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -108,83 +122,114 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
   const int64_t start = valid ? a.offsets[b] : 0;
   const int T = valid ? (int)(a.offsets[b + 1] - start) : 0;
   const R* __restrict__ y0g = reinterpret_cast<const R*>(a.y0) + start;
-  const R* __restrict__ y1g = a.y1 ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
-  const bool two = a.n_streams > 1;
+  const bool two = VF::TWO && a.n_streams > 1;
+  const R* __restrict__ y1g = two ? reinterpret_cast<const R*>(a.y1) + start : y0g;
 
-  // column j of log A and the state's emission record
+  // column j of log A and the state's emission parameters, in registers
   R la[K];
   const int jj = valid ? j : 0;
 #pragma unroll
   for (int i = 0; i < K; ++i) la[i] = (R)md->log_A[i * K + jj];
-  const loghmm_emission_t e0 = md->em[0][jj];
-  loghmm_emission_t e1;
-  if (two) e1 = md->em[1][jj];
+  ExactEm<R, VF::F0> em0;
+  em0.load(md->em[0][jj]);
+  ExactEm<R, VF::F1> em1;
+  if (two) em1.load(md->em[1][jj]);
+  else em1.fam = LOGHMM_FAM_NONE;
   bool oob = false;
-  auto logb = [&](int t) -> R {
-    const R v0 = y0g[t];
-    R v = exact_logb<R>(e0, v0, a.lut, a.lut_n, oob);
-    if (two) v = N::add(v, exact_logb<R>(e1, y1g[t], a.lut, a.lut_n, oob));
-    return v;
-  };
+  const double* lut = a.lut;
+  const int lut_n = a.lut_n;
 
   int Tmax = T;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) Tmax = max(Tmax, __shfl_xor_sync(kFull, Tmax, o));
+  const int Tlast = T > 0 ? T - 1 : 0;
 
   // ---- forward max-plus recursion ---------------------------------------
   R delta = N::ninf();
-  if (valid && T > 0) delta = N::add((R)md->log_pi[jj], logb(0));
-  if (valid && T > 0 && a.back) a.back[start * K + j] = 0;
-  unsigned pw[NP > 0 ? NP : 1];
+  if (T > 0) {
+    R lb0 = em0.eval(y0g[0], lut, lut_n, oob);
+    if (two) lb0 = N::add(lb0, em1.eval(y1g[0], lut, lut_n, oob));
+    delta = N::add((R)md->log_pi[jj], lb0);
+  }
+
+  // One recursion step: every lane executes it (no divergence around the
+  // shuffles / ballots); lanes past their sequence end keep their score.
+  // Lane 0 stores the step's bit-planes (one shared-memory store per step).
+  uint32_t* pl_st = planes;
+  auto step = [&](int t, R yv0, R yv1) {
+    R lb = em0.eval(yv0, lut, lut_n, oob);
+    if (two) lb = N::add(lb, em1.eval(yv1, lut, lut_n, oob));
+    R cand[K];
 #pragma unroll
-  for (int p = 0; p < (NP > 0 ? NP : 1); ++p) pw[p] = 0;
+    for (int i = 0; i < K; ++i) cand[i] = N::add(__shfl_sync(kFull, delta, g * K + i), la[i]);
+    R best;
+    int bi;
+    ArgMax<R, 0, K>::run(cand, best, bi);
+    delta = t < T ? N::add(best, lb) : delta;
+    unsigned w[NP > 0 ? NP : 1];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) w[p] = __ballot_sync(kFull, (bi >> p) & 1);
+    if (lane == 0) {
+      if constexpr (NP == 1) {
+        pl_st[(size_t)t] = w[0];
+      } else if constexpr (NP == 2) {
+        *reinterpret_cast<uint2*>(pl_st + (size_t)t * 2) = make_uint2(w[0], w[1]);
+      } else if constexpr (NP == 3) {
+#pragma unroll
+        for (int p = 0; p < 3; ++p) pl_st[(size_t)t * 3 + p] = w[p];
+      }
+    }
+  };
 
   constexpr int U = 8;
-  R ycur[U], ynx[U];
-  auto yload = [&](int t) -> R {
-    const int tt = t < T ? t : (T > 0 ? T - 1 : 0);
-    return valid && T > 0 ? y0g[tt] : R(0);
-  };
+  R y0c[U], y0n[U], y1c[U], y1n[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) ynx[u] = yload(1 + u);
+  for (int u = 0; u < U; ++u) {
+    const int tt = min(1 + u, Tlast);
+    y0n[u] = y0g[tt];
+    y1n[u] = two ? y1g[tt] : R(0);
+  }
+  int t = 1;
 #pragma unroll 1
-  for (int tb = 1; tb < Tmax; tb += U) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) ycur[u] = ynx[u];
-#pragma unroll
-    for (int u = 0; u < U; ++u) ynx[u] = yload(tb + U + u);
+  for (; t + U <= Tmax; t += U) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int t = tb + u;
-      if (t < Tmax) {
-        const bool act = valid && t < T;
-        R lb;
-        {
-          R v = exact_logb<R>(e0, ycur[u], a.lut, a.lut_n, oob);
-          if (two) v = N::add(v, exact_logb<R>(e1, act ? y1g[t] : R(0), a.lut, a.lut_n, oob));
-          lb = v;
-        }
-        R cand[K];
+      y0c[u] = y0n[u];
+      y1c[u] = y1n[u];
+    }
 #pragma unroll
-        for (int i = 0; i < K; ++i) cand[i] = N::add(__shfl_sync(kFull, delta, g * K + i), la[i]);
-        R best;
-        int bi;
-        ArgMax<R, 0, K>::run(cand, best, bi);
-        const R nd = N::add(best, lb);
-        if (act) delta = nd;
-        const unsigned bpv = act ? (unsigned)bi : 0u;
-        if (act && a.back) a.back[(start + t) * K + j] = (uint8_t)bpv;
+    for (int u = 0; u < U; ++u) {
+      const int tt = min(t + U + u, Tlast);
+      y0n[u] = y0g[tt];
+      y1n[u] = two ? y1g[tt] : R(0);
+    }
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          const unsigned w = __ballot_sync(kFull, (bpv >> p) & 1u);
-          if (lane == (t & 31)) pw[p] = w;
-        }
-        if ((t & 31) == 31 || t == Tmax - 1) {
-          const int tw = (t & ~31) + lane;
-          if (tw <= t) {
+    for (int u = 0; u < U; ++u) step(t + u, y0c[u], y1c[u]);
+  }
+#pragma unroll 1
+  for (; t < Tmax; ++t) {
+    const int tt = min(t, Tlast);
+    step(t, y0g[tt], two ? y1g[tt] : R(0));
+  }
+
+  __syncwarp();
+  // optional byte table of backpointers (tests), rebuilt from the planes
+  if (a.back != nullptr) {
+#pragma unroll 1
+    for (int gg = 0; gg < G; ++gg) {
+      const int64_t bb = warp_id * G + gg;
+      if (bb >= a.B) break;
+      const int Tg = __shfl_sync(kFull, T, gg * K);
+      const int64_t sg = __shfl_sync(kFull, start, gg * K);
+      for (int t = lane; t < Tg; t += kWarp) {
 #pragma unroll
-            for (int p = 0; p < NP; ++p) planes[(size_t)tw * NP + p] = pw[p];
+        for (int jx = 0; jx < K; ++jx) {
+          unsigned v8 = 0;
+          if (t >= 1) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) v8 |= ((planes[(size_t)t * NP + p] >> (gg * K + jx)) & 1u) << p;
           }
+          a.back[(sg + t) * K + jx] = (uint8_t)v8;
         }
       }
     }
