@@ -174,7 +174,7 @@ int32_t loghmm_reduce_stats(const double* partials, const double* ll, int64_t B,
  * m_step_transitions; writes the next model block to model_out and per-state
  * status words to status[n_streams*K] (index s*K + j).
  * n_sequences is B (pi is the mean of first gammas, training.py:117).
- * guard_state: n_streams*K*8 doubles of scratch for the Student-t guard. */
+ * guard_state: n_streams*K*16 doubles of scratch (Student-t guard, variance pass). */
 enum loghmm_mstep_status {
   LOGHMM_MS_UPDATED = 0,
   LOGHMM_MS_COLLAPSED = 1,           /* total weight < epsilon: kept  */
@@ -190,8 +190,21 @@ enum loghmm_mstep_status {
 };
 int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64_t n_sequences,
                      double collapse_epsilon, double nu_ceiling, double nu_tol, int32_t max_newton,
-                     loghmm_model_t* model_out, int32_t* status, double* guard_state,
-                     void* stream);
+                     double var_ratio, loghmm_model_t* model_out, int32_t* status,
+                     double* guard_state, void* stream);
+
+/* Exact second pass for the variance-type statistics (distributions.py:616-620
+ * two-pass variance, :1051 ECME scale).  The E-step accumulates sums shifted
+ * about the current parameters; when the M-step finds the new mean moved by
+ * more than sqrt(var_ratio) standard deviations from that shift (so the
+ * one-pass difference would lose precision) it flags the state and this call
+ * recomputes sum_w (y - mean)^2 from y and gamma and finishes the fit.  Cheap
+ * no-op when nothing is flagged.  Call after loghmm_mstep, before
+ * loghmm_student_guard. */
+int32_t loghmm_variance_pass(int32_t dtype, loghmm_model_t* model_out, const void* y,
+                             const void* gamma, int64_t N, int32_t K, int32_t stream_index,
+                             const double* guard_state, int32_t* status, void* workspace,
+                             size_t workspace_bytes, void* stream);
 
 /* Student-t ECME likelihood guard (distributions.py:1080-1086): one data pass
  * over y and gamma evaluates sum_w log1p(z^2/nu) at the base nu0 and at

@@ -3,6 +3,7 @@
 // Host-side argument checking, launch geometry, shared-memory carve and
 // dtype / K / family dispatch.  No allocation, no global mutable state.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "hmm_large.cuh"
@@ -144,6 +145,32 @@ static cudaError_t dispatch_vit_small(int K, const VitArgs& a, int cfg, bool gl,
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Forward-backward decomposition: meet-in-the-middle (hmm_fbm.cuh) when the
+// batch alone fills the GPU, else the chunked scan over T (hmm_fb.cuh).
+// LOGHMM_FB_ALGO=chunked|mitm forces one (tests exercise both).
+static bool use_mitm(int K, int64_t B) {
+  if (K > 8 || K < 2) return false;
+  const char* env = getenv("LOGHMM_FB_ALGO");
+  if (env && strcmp(env, "chunked") == 0) return false;
+  if (env && strcmp(env, "mitm") == 0) return true;
+  return B >= 1024;
+}
+
+static int64_t mitm_kp(int K) { return K >= 2 ? 2 * ((K + 1) / 2) : K; }
+
+template <typename R>
+static cudaError_t dispatch_fb_mitm(int K, const FBMArgs& a, int cfg, dim3 grid, cudaStream_t st) {
+  switch (K) {
+    case 2: return launch_fb_mitm<R, 2>(a, cfg, grid, fb_mitm_smem<R, 2>(), st);
+    case 3: return launch_fb_mitm<R, 3>(a, cfg, grid, fb_mitm_smem<R, 3>(), st);
+    case 4: return launch_fb_mitm<R, 4>(a, cfg, grid, fb_mitm_smem<R, 4>(), st);
+    case 5: return launch_fb_mitm<R, 5>(a, cfg, grid, fb_mitm_smem<R, 5>(), st);
+    case 6: return launch_fb_mitm<R, 6>(a, cfg, grid, fb_mitm_smem<R, 6>(), st);
+    case 7: return launch_fb_mitm<R, 7>(a, cfg, grid, fb_mitm_smem<R, 7>(), st);
+    default: return launch_fb_mitm<R, 8>(a, cfg, grid, fb_mitm_smem<R, 8>(), st);
+  }
+}
+
 }  // namespace lhmm
 
 using namespace lhmm;
@@ -163,6 +190,11 @@ size_t loghmm_fb_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N,
   (void)B;
   const int esz = dtype == LOGHMM_F64 ? 8 : 4;
   if (K > 8) return align256((size_t)N * K * esz);
+  if (use_mitm(K, B)) {
+    const int64_t G = 16;
+    const int64_t Bp = ((B + G - 1) / G) * G;
+    return align256((size_t)max_T * Bp * mitm_kp(K) * esz);
+  }
   FBGeom g = fb_geom(K, esz, 2, max_T);
   return g.global ? align256((size_t)N * K * esz) : 0;
 }
@@ -236,7 +268,32 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
   const int cfg = cfg_of(h_desc, &fams);
   a.stream_fams = fams;
   cudaError_t e;
-  if (K <= 8) {
+  if (use_mitm(K, B)) {
+    FBMArgs m{};
+    m.model = model;
+    m.y0 = a.y0;
+    m.y1 = a.y1;
+    m.offsets = offsets;
+    m.B = B;
+    m.lut = lgamma_lut;
+    m.lut_n = lut_n;
+    m.n_streams = a.n_streams;
+    m.log_alpha = log_alpha;
+    m.log_beta = log_beta;
+    m.gamma = gamma;
+    m.xi = xi;
+    m.ll = ll;
+    m.partials = partials;
+    m.flags = flags;
+    m.ws = workspace;
+    const int64_t G = 16;
+    const int64_t nblk = (B + G - 1) / G;
+    m.ws_bstride = nblk * G * mitm_kp(K);
+    m.stats_width = a.stats_width;
+    dim3 grid((unsigned)nblk);
+    e = dtype == LOGHMM_F64 ? dispatch_fb_mitm<double>(K, m, cfg, grid, st)
+                            : dispatch_fb_mitm<float>(K, m, cfg, grid, st);
+  } else if (K <= 8) {
     FBGeom g = fb_geom(K, esz, h_desc->n_streams, max_T);
     a.L_align = g.L_align;
     a.Lmax = g.Lmax;
@@ -327,13 +384,36 @@ int32_t loghmm_reduce_stats(const double* partials, const double* ll, int64_t B,
 
 int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64_t n_sequences,
                      double collapse_epsilon, double nu_ceiling, double nu_tol, int32_t max_newton,
-                     loghmm_model_t* model_out, int32_t* status, double* guard_state,
-                     void* stream) {
+                     double var_ratio, loghmm_model_t* model_out, int32_t* status,
+                     double* guard_state, void* stream) {
   if (!model_in || !totals || !model_out || !status || !guard_state || n_sequences < 1)
     return LOGHMM_EINVAL;
   mstep_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(model_in, totals, n_sequences,
                                                     collapse_epsilon, nu_ceiling, nu_tol,
-                                                    max_newton, model_out, status, guard_state);
+                                                    max_newton, model_out, status, guard_state,
+                                                    var_ratio);
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+int32_t loghmm_variance_pass(int32_t dtype, loghmm_model_t* model_out, const void* y,
+                             const void* gamma, int64_t N, int32_t K, int32_t stream_index,
+                             const double* guard_state, int32_t* status, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  if (!model_out || !y || !gamma || !guard_state || !status || K < 1) return LOGHMM_EINVAL;
+  if (workspace_bytes < loghmm_guard_workspace_bytes(K, N)) return LOGHMM_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nblocks = 148 * 4;
+  double* part = (double*)workspace;
+  if (dtype == LOGHMM_F64)
+    variance_pass_kernel<double><<<nblocks, 256, 0, st>>>((const double*)y, (const double*)gamma, N,
+                                                          K, stream_index, model_out, guard_state,
+                                                          part);
+  else
+    variance_pass_kernel<float><<<nblocks, 256, 0, st>>>((const float*)y, (const float*)gamma, N, K,
+                                                         stream_index, model_out, guard_state,
+                                                         part);
+  variance_finish_kernel<<<1, 64, 0, st>>>(model_out, K, stream_index, guard_state, part, nblocks,
+                                           status);
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 

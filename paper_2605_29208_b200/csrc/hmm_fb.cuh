@@ -221,6 +221,43 @@ __device__ __forceinline__ void normalise_vec(R (&v)[K], double& off) {
   }
 }
 
+// Power-of-two normalisation with the offset kept in log2 units (exact).
+template <typename R, int K>
+__device__ __forceinline__ void normalise_mat2(R (&Z)[K][K], double& off2) {
+  R m = Z[0][0];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int c = 0; c < K; ++c) m = rmax(m, Z[r][c]);
+  if (m > R(0)) {
+    int e;
+    const R s = Num<R>::pow2_scale(m, e);
+    off2 += (double)e;
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+#pragma unroll
+      for (int c = 0; c < K; ++c) Z[r][c] *= s;
+  } else {
+    off2 = -CUDART_INF;
+  }
+}
+
+template <typename R, int K>
+__device__ __forceinline__ void normalise_vec2(R (&v)[K], double& off2) {
+  R m = v[0];
+#pragma unroll
+  for (int i = 1; i < K; ++i) m = rmax(m, v[i]);
+  if (m > R(0)) {
+    int e;
+    const R s = Num<R>::pow2_scale(m, e);
+    off2 += (double)e;
+#pragma unroll
+    for (int i = 0; i < K; ++i) v[i] *= s;
+  } else {
+    off2 = -CUDART_INF;
+  }
+}
+
 template <typename R, int K>
 __device__ __forceinline__ void shfl_mat(R (&Z)[K][K], double& off, const R (&X)[K][K], double xo,
                                          int delta, bool up) {
@@ -492,14 +529,20 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
   bool nan_seen = false;
   int dead_t = INT_MAX;
 
+  // All recursions below work in log2 units (ex2/lg2 on the MUFU, offsets
+  // exact in base 2); outputs are converted to natural logs when staged.
+  constexpr R kL2E = R(1.4426950408889634);
+  constexpr R kLN2 = R(0.6931471805599453);
+  constexpr double kLN2d = 0.6931471805599453094;
+
   // ---- phase 1: chunk transfer operator --------------------------------
   R Mop[K][K];
 #pragma unroll
   for (int r = 0; r < K; ++r)
 #pragma unroll
     for (int c = 0; c < K; ++c) Mop[r][c] = r == c ? R(1) : R(0);
-  double moff = 0.0;
-  R seed_u[K];  // lane 0: log pi + log b_0
+  double moff = 0.0;  // log2 offset of Mop
+  R seed_u[K];        // lane 0: log2(pi) + log2 b_0
 #pragma unroll
   for (int j = 0; j < K; ++j) seed_u[j] = N::ninf();
   {
@@ -520,31 +563,35 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
       }
       if (t == 0) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) seed_u[j] = lpi[j] + lb[j];
+        for (int j = 0; j < K; ++j) seed_u[j] = (lpi[j] + lb[j]) * kL2E;
         continue;
       }
       const bool finite_m = m > N::ninf();
+      const R m2 = m * kL2E;
       R bt[K];
 #pragma unroll
-      for (int j = 0; j < K; ++j) bt[j] = finite_m ? N::fexp(lb[j] - m) : R(0);
-      R AD[K][K];
-#pragma unroll
-      for (int i = 0; i < K; ++i)
-#pragma unroll
-        for (int j = 0; j < K; ++j) AD[i][j] = Am[i][j] * bt[j];
+      for (int j = 0; j < K; ++j) bt[j] = finite_m ? N::fex2(fma(lb[j], kL2E, -m2)) : R(0);
       R Nw[K][K];
-      matmul<R, K>(Mop, AD, Nw);
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          R acc = Mop[r][0] * Am[0][c];
+#pragma unroll
+          for (int i = 1; i < K; ++i) acc = fma(Mop[r][i], Am[i][c], acc);
+          Nw[r][c] = acc * bt[c];
+        }
 #pragma unroll
       for (int r = 0; r < K; ++r)
 #pragma unroll
         for (int c = 0; c < K; ++c) Mop[r][c] = Nw[r][c];
-      moff += finite_m ? (double)m : -CUDART_INF;
+      moff += finite_m ? (double)m2 : -CUDART_INF;
       if (++cnt == nn) {
         cnt = 0;
-        normalise_mat<R, K>(Mop, moff);
+        normalise_mat2<R, K>(Mop, moff);
       }
     }
-    normalise_mat<R, K>(Mop, moff);
+    normalise_mat2<R, K>(Mop, moff);
   }
 
   // ---- phase 2a: forward scan (inclusive prefix of operators) -------------
@@ -571,7 +618,7 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
 #pragma unroll
           for (int c = 0; c < K; ++c) Q[r][c] = Z[r][c];
         qo += po;
-        normalise_mat<R, K>(Q, qo);
+        normalise_mat2<R, K>(Q, qo);
       }
     }
     // seed vector alpha_0 (lane 0), broadcast
@@ -581,12 +628,11 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
     R sv[K];
     const bool sfin = sm > N::ninf();
 #pragma unroll
-    for (int j = 0; j < K; ++j) sv[j] = sfin ? N::fexp(seed_u[j] - sm) : R(0);
+    for (int j = 0; j < K; ++j) sv[j] = sfin ? N::fex2(seed_u[j] - sm) : R(0);
     double so = sfin ? (double)sm : -CUDART_INF;
 #pragma unroll
     for (int j = 0; j < K; ++j) sv[j] = __shfl_sync(kFull, sv[j], 0);
     so = __shfl_sync(kFull, so, 0);
-    // v_c = seed * Q_c
     R v[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
@@ -596,24 +642,21 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
       v[c] = acc;
     }
     double vo = so + qo;
-    normalise_vec<R, K>(v, vo);
-    // log-likelihood from lane 31
+    normalise_vec2<R, K>(v, vo);
     R vs = v[0];
 #pragma unroll
     for (int j = 1; j < K; ++j) vs += v[j];
-    double llv = vo + (double)N::flog(vs);
+    double llv = (vo + (double)N::flg2(vs)) * kLN2d;
     if (!(vs > R(0))) llv = -CUDART_INF;
     LL = __shfl_sync(kFull, llv, kWarp - 1);
-    // entering vector for lane c = v_{c-1}
 #pragma unroll
     for (int j = 0; j < K; ++j) a_in[j] = __shfl_up_sync(kFull, v[j], 1);
     lam_in = __shfl_up_sync(kFull, vo, 1);
-    // rescale to max 1 exactly representable (pow2 normalised already)
   }
 
   // ---- phase 2b: backward scan (inclusive suffix of operators) ------------
-  R r_ex[K];
-  double rho_ex;
+  R b_ex[K];  // beta~ at the chunk's last step (linear, pow2-normalised)
+  double rho_ex;  // log2 offset
   {
     R S[K][K];
 #pragma unroll
@@ -634,7 +677,7 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
 #pragma unroll
           for (int c = 0; c < K; ++c) S[r][c] = Z[r][c];
         so += yo;
-        normalise_mat<R, K>(S, so);
+        normalise_mat2<R, K>(S, so);
       }
     }
     R z[K];
@@ -645,98 +688,94 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
       for (int c = 1; c < K; ++c) acc += S[r][c];
       z[r] = acc;
     }
-    double zo = so;
-    R e[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) e[j] = __shfl_down_sync(kFull, z[j], 1);
-    double eo = __shfl_down_sync(kFull, zo, 1);
+    for (int j = 0; j < K; ++j) b_ex[j] = __shfl_down_sync(kFull, z[j], 1);
+    rho_ex = __shfl_down_sync(kFull, so, 1);
     if (lane == kWarp - 1) {
 #pragma unroll
-      for (int j = 0; j < K; ++j) e[j] = R(1);
-      eo = 0.0;
+      for (int j = 0; j < K; ++j) b_ex[j] = R(1);
+      rho_ex = 0.0;
     }
-    R me = e[0];
-#pragma unroll
-    for (int j = 1; j < K; ++j) me = rmax(me, e[j]);
-    if (me > R(0)) {
-      const R lme = N::flog(me);
-#pragma unroll
-      for (int j = 0; j < K; ++j) r_ex[j] = e[j] > R(0) ? N::flog(e[j]) - lme : N::ninf();
-      rho_ex = eo + (double)lme;
-    } else {
-#pragma unroll
-      for (int j = 0; j < K; ++j) r_ex[j] = R(0);
-      rho_ex = -CUDART_INF;
-    }
+    normalise_vec2<R, K>(b_ex, rho_ex);
   }
 
-  // Row-major base of this warp's alpha store.
+  // Row-major base of this warp's beta~ store.
   R* aw = kGlobal ? reinterpret_cast<R*>(a.alpha_ws) + (start + t0) * K : abuf + lane * a.a_pitch;
   const bool vec_ok = ((start * K * (int64_t)sizeof(R)) % 16 == 0) &&
                       ((L * K * (int)sizeof(R)) % 16 == 0);
   FlushPlan<R, K> fplan;
   fplan.init(lane, start, L, T, a.s_pitch, vec_ok);
 
-  // ---- phase 3a: forward re-sweep -----------------------------------------
+  // ---- phase 3a: backward re-sweep (linear), writes log_beta, keeps beta~ --
   R* __restrict__ outA = reinterpret_cast<R*>(a.log_alpha);
+  R* __restrict__ outB = reinterpret_cast<R*>(a.log_beta);
+  R* __restrict__ outG = reinterpret_cast<R*>(a.gamma);
+  R* __restrict__ outX = reinterpret_cast<R*>(a.xi);
   {
-    R av[K];
-    double lam = lam_in;
+    R bt[K];
+    double rho = rho_ex;
 #pragma unroll
-    for (int j = 0; j < K; ++j) av[j] = a_in[j];
+    for (int j = 0; j < K; ++j) bt[j] = b_ex[j];
+    const int s_top = len - 1;
+    int cnt = 0;
 #pragma unroll 1
-    for (int s = 0; s < L; ++s) {
-      const int t = t0 + s;
-      if (s < len) {
-        ObsFeat<R> f0, f1;
-        R lb[K], u[K];
-        em.eval(yat0(s), yat1(s), f0, f1, lb, oob);
-        if (t == 0) {
-#pragma unroll
-          for (int j = 0; j < K; ++j) u[j] = lpi[j] + lb[j];
-          lam = 0.0;
-        } else {
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            R acc = av[0] * Am[0][c];
-#pragma unroll
-            for (int i = 1; i < K; ++i) acc = fma(av[i], Am[i][c], acc);
-            u[c] = N::flog(acc) + lb[c];
-          }
-        }
-        if (outA) {
-          const R lr = (R)lam;
+    for (int s = L - 1; s >= 0; --s) {
+      if (s == s_top) {
+        VecIO<R, K>::st(aw + s * K, bt);
+        if (outB) {
+          const R rr = (R)rho;
           R o[K];
 #pragma unroll
-          for (int j = 0; j < K; ++j) o[j] = lr + u[j];
+          for (int j = 0; j < K; ++j) o[j] = (rr + N::flg2(bt[j])) * kLN2;
           VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
         }
-        R M = u[0];
+      } else if (s < s_top) {
+        // beta_s = A (b_{s+1} . beta_{s+1})
+        ObsFeat<R> f0, f1;
+        R lb[K];
+        em.eval(yat0(s + 1), yat1(s + 1), f0, f1, lb, oob);
+        R m = lb[0];
 #pragma unroll
-        for (int j = 1; j < K; ++j) M = rmax(M, u[j]);
-        if (M > N::ninf()) {
+        for (int j = 1; j < K; ++j) m = rmax(m, lb[j]);
+        const bool fin = m > N::ninf();
+        const R m2 = m * kL2E;
+        R w[K];
 #pragma unroll
-          for (int j = 0; j < K; ++j) av[j] = N::fexp(u[j] - M);
-          lam += (double)M;
-        } else {
+        for (int j = 0; j < K; ++j) w[j] = (fin ? N::fex2(fma(lb[j], kL2E, -m2)) : R(0)) * bt[j];
+        R q[K];
 #pragma unroll
-          for (int j = 0; j < K; ++j) av[j] = R(0);
+        for (int i = 0; i < K; ++i) {
+          R acc = Am[i][0] * w[0];
+#pragma unroll
+          for (int j = 1; j < K; ++j) acc = fma(Am[i][j], w[j], acc);
+          q[i] = acc;
         }
-        VecIO<R, K>::st(aw + s * (kGlobal ? K : K), av);
+        rho += fin ? (double)m2 : 0.0;
+        if (outB) {
+          const R rr = (R)rho;
+          R o[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) o[j] = (rr + N::flg2(q[j])) * kLN2;
+          VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) bt[j] = q[j];
+        if (++cnt == nn) {
+          cnt = 0;
+          normalise_vec2<R, K>(bt, rho);
+        }
+        VecIO<R, K>::st(aw + s * K, bt);
       }
-      if (outA && ((s % kSlab) == kSlab - 1 || s == L - 1)) {
+      if ((s % kSlab) == 0 && outB) {
         __syncwarp();
-        flush_slab<R, K>(outA, stA, fplan, a.s_pitch, start, L, T, s - (s % kSlab), lane);
+        flush_slab<R, K>(outB, stA, fplan, a.s_pitch, start, L, T, s, lane);
         __syncwarp();
       }
     }
   }
-  if (kGlobal) __syncwarp();
+  __syncwarp();
 
-  // ---- phase 3b: backward re-sweep with posteriors and statistics --------
-  R* __restrict__ outB = reinterpret_cast<R*>(a.log_beta);
-  R* __restrict__ outG = reinterpret_cast<R*>(a.gamma);
-  R* __restrict__ outX = reinterpret_cast<R*>(a.xi);
+  // ---- phase 3b: forward re-sweep fused with posteriors and statistics -----
   R X[K][K];
   R gtot[K], g0[K];
   R st[TR::S][K][LOGHMM_NSLOT];
@@ -752,134 +791,118 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
       for (int q = 0; q < LOGHMM_NSLOT; ++q) st[s][i][q] = R(0);
   }
   {
-    R r[K];
-    double rho = rho_ex;
+    R av[K];
+    double lam = lam_in;
 #pragma unroll
-    for (int j = 0; j < K; ++j) r[j] = r_ex[j];
-    const int s_top = len - 1;
-    // Emission of the step above the current pair, carried between iterations
-    // so every step is evaluated once.
-    ObsFeat<R> cf0, cf1;
-    R clb[K];
+    for (int j = 0; j < K; ++j) av[j] = a_in[j];
+    int cnt = 0;
 #pragma unroll 1
-    for (int s = L - 1; s >= -1; --s) {
-      if (len > 0 && s == s_top) {
-        // last step of the chunk: beta from the scan
-        const int t = t0 + s;
-        em.eval(yat0(s), yat1(s), cf0, cf1, clb, oob);
-        R q[K], av[K], g[K];
+    for (int s = 0; s < L; ++s) {
+      const int t = t0 + s;
+      if (s < len) {
+        ObsFeat<R> f0, f1;
+        R lb[K];
+        em.eval(yat0(s), yat1(s), f0, f1, lb, oob);
+        R bet[K];
+        VecIO<R, K>::ld(aw + s * K, bet);
+        R g[K];
+        if (t == 0) {
+          R u[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) q[j] = N::fexp(r[j]);
-        VecIO<R, K>::ld(aw + s * K, av);
-        R Z = R(0);
+          for (int j = 0; j < K; ++j) u[j] = (lpi[j] + lb[j]) * kL2E;
+          R M = u[0];
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          g[j] = av[j] * q[j];
-          Z += g[j];
-        }
-        const R iz = N::frcp(Z);
+          for (int j = 1; j < K; ++j) M = rmax(M, u[j]);
+          const bool fin = M > N::ninf();
+          if (outA) {
+            R o[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) g[j] *= iz;
-        if (outB) {
-          const R rr = (R)rho;
-          R o[K];
+            for (int j = 0; j < K; ++j) o[j] = u[j] * kLN2;
+            VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
+          }
 #pragma unroll
-          for (int j = 0; j < K; ++j) o[j] = rr + r[j];
-          VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
+          for (int j = 0; j < K; ++j) av[j] = fin ? N::fex2(u[j] - M) : R(0);
+          lam = fin ? (double)M : -CUDART_INF;
+          R Z = R(0);
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            g[j] = av[j] * bet[j];
+            Z += g[j];
+          }
+          const R iz = N::frcp(Z);
+#pragma unroll
+          for (int j = 0; j < K; ++j) g[j] *= iz;
+#pragma unroll
+          for (int j = 0; j < K; ++j) g0[j] = g[j];
+        } else {
+          R m = lb[0];
+#pragma unroll
+          for (int j = 1; j < K; ++j) m = rmax(m, lb[j]);
+          const bool fin = m > N::ninf();
+          const R m2 = m * kL2E;
+          R bb[K], p[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) bb[j] = fin ? N::fex2(fma(lb[j], kL2E, -m2)) : R(0);
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            R acc = av[0] * Am[0][c];
+#pragma unroll
+            for (int i = 1; i < K; ++i) acc = fma(av[i], Am[i][c], acc);
+            p[c] = acc;
+          }
+          if (outA) {
+            const R lr = (R)lam;
+            R o[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) o[j] = fma(lb[j], kL2E, lr + N::flg2(p[j])) * kLN2;
+            VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
+          }
+          // pair (t-1, t): xi_{t-1}(i,j) = a_{t-1}[i] A_ij bb_j beta~_t[j] / Z
+          R v[K];
+          R Z = R(0);
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            v[j] = bb[j] * bet[j];
+            Z = fma(p[j], v[j], Z);
+          }
+          const R iz = N::frcp(Z);
+          R cv[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            cv[j] = v[j] * iz;
+            g[j] = p[j] * cv[j];
+          }
+#pragma unroll
+          for (int i = 0; i < K; ++i)
+#pragma unroll
+            for (int j = 0; j < K; ++j) X[i][j] = fma(av[i], cv[j], X[i][j]);
+          if (outX) {
+            R* xr = outX + ((start - b) + (t - 1)) * (int64_t)(K * K);
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+#pragma unroll
+              for (int j = 0; j < K; ++j) xr[i * K + j] = av[i] * Am[i][j] * cv[j];
+          }
+#pragma unroll
+          for (int j = 0; j < K; ++j) av[j] = p[j] * bb[j];
+          lam += fin ? (double)m2 : 0.0;
+          if (++cnt == nn) {
+            cnt = 0;
+            normalise_vec2<R, K>(av, lam);
+          }
         }
         if (outG) VecIO<R, K>::st(stB + lane * a.s_pitch + (s % kSlab) * K, g);
-        stats_step<R, K, CFG>(st, g, em, cf0, cf1);
+        stats_step<R, K, CFG>(st, g, em, f0, f1);
         if (t < T - 1) {
 #pragma unroll
           for (int j = 0; j < K; ++j) gtot[j] += g[j];
         }
-        if (t == 0) {
-#pragma unroll
-          for (int j = 0; j < K; ++j) g0[j] = g[j];
-        }
-      } else if (len > 0 && s < s_top && (t0 + s) >= 0) {
-        // pair (t0+s, t0+s+1); clb holds log b at t0+s+1
-        const int tl = t0 + s;
-        R u[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) u[j] = clb[j] + r[j];
-        R M = u[0];
-#pragma unroll
-        for (int j = 1; j < K; ++j) M = rmax(M, u[j]);
-        const bool fin = M > N::ninf();
-        R w[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) w[j] = fin ? N::fexp(u[j] - M) : R(0);
-        R q[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          R acc = Am[i][0] * w[0];
-#pragma unroll
-          for (int j = 1; j < K; ++j) acc = fma(Am[i][j], w[j], acc);
-          q[i] = acc;
-        }
-        R ap[K];
-        if (s >= 0) {
-          VecIO<R, K>::ld(aw + s * K, ap);
-        } else {
-#pragma unroll
-          for (int j = 0; j < K; ++j) ap[j] = a_in[j];
-        }
-        R Z = R(0);
-#pragma unroll
-        for (int i = 0; i < K; ++i) Z = fma(ap[i], q[i], Z);
-        const R iz = N::frcp(Z);
-        R ai[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) ai[i] = ap[i] * iz;
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-#pragma unroll
-          for (int j = 0; j < K; ++j) X[i][j] = fma(ai[i], w[j], X[i][j]);
-        if (outX) {
-          R* xr = outX + ((start - b) + tl) * (int64_t)(K * K);
-#pragma unroll
-          for (int i = 0; i < K; ++i)
-#pragma unroll
-            for (int j = 0; j < K; ++j) xr[i * K + j] = ai[i] * Am[i][j] * w[j];
-        }
-        R lq[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) lq[i] = q[i] > R(0) ? N::flog(q[i]) : N::ninf();
-        if (s >= 0) {
-          if (outB) {
-            const R rr = (R)(rho + (fin ? (double)M : 0.0));
-            R o[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) o[j] = rr + lq[j];
-            VecIO<R, K>::st(stA + lane * a.s_pitch + (s % kSlab) * K, o);
-          }
-          R g[K];
-#pragma unroll
-          for (int j = 0; j < K; ++j) g[j] = ai[j] * q[j];
-          if (outG) VecIO<R, K>::st(stB + lane * a.s_pitch + (s % kSlab) * K, g);
-          em.eval(yat0(s), yat1(s), cf0, cf1, clb, oob);
-          stats_step<R, K, CFG>(st, g, em, cf0, cf1);
-#pragma unroll
-          for (int j = 0; j < K; ++j) gtot[j] += g[j];
-          if (tl == 0) {
-#pragma unroll
-            for (int j = 0; j < K; ++j) g0[j] = g[j];
-          }
-        }
-        R mq = lq[0];
-#pragma unroll
-        for (int j = 1; j < K; ++j) mq = rmax(mq, lq[j]);
-        if (mq > N::ninf()) {
-#pragma unroll
-          for (int j = 0; j < K; ++j) r[j] = lq[j] - mq;
-          rho += (fin ? (double)M : 0.0) + (double)mq;
-        }
       }
-      if (s >= 0 && (s % kSlab) == 0 && (outB || outG)) {
+      if (((s % kSlab) == kSlab - 1 || s == L - 1) && (outA || outG)) {
         __syncwarp();
-        if (outB) flush_slab<R, K>(outB, stA, fplan, a.s_pitch, start, L, T, s, lane);
-        if (outG) flush_slab<R, K>(outG, stB, fplan, a.s_pitch, start, L, T, s, lane);
+        const int sb = s - (s % kSlab);
+        if (outA) flush_slab<R, K>(outA, stA, fplan, a.s_pitch, start, L, T, sb, lane);
+        if (outG) flush_slab<R, K>(outG, stB, fplan, a.s_pitch, start, L, T, sb, lane);
         __syncwarp();
       }
     }

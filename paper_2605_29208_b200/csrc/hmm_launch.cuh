@@ -3,6 +3,7 @@
 #pragma once
 
 #include "hmm_fb.cuh"
+#include "hmm_fbm.cuh"
 #include "hmm_viterbi.cuh"
 
 namespace lhmm {
@@ -69,16 +70,47 @@ cudaError_t launch_vit_small(const VitArgs& a, int cfg, bool global, dim3 grid, 
                 : launch_vit_cfg<R, K, false>(a, cfg, grid, block, smem, st);
 }
 
-#define LHMM_DECLARE_INST(R, K)                                                              \
+template <typename R, int K, int CFG>
+static cudaError_t launch_fbm_one(const FBMArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+  auto fn = fb_mitm_kernel<R, K, CFG>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<grid, 64, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename R, int K>
+cudaError_t launch_fb_mitm(const FBMArgs& a, int cfg, dim3 grid, size_t smem, cudaStream_t st) {
+  switch (cfg) {
+    case kCfgGauss: return launch_fbm_one<R, K, kCfgGauss>(a, grid, smem, st);
+    case kCfgStudent: return launch_fbm_one<R, K, kCfgStudent>(a, grid, smem, st);
+    case kCfgGamma: return launch_fbm_one<R, K, kCfgGamma>(a, grid, smem, st);
+    case kCfgVonMises: return launch_fbm_one<R, K, kCfgVonMises>(a, grid, smem, st);
+    case kCfgPoisson: return launch_fbm_one<R, K, kCfgPoisson>(a, grid, smem, st);
+    case kCfgGammaVM: return launch_fbm_one<R, K, kCfgGammaVM>(a, grid, smem, st);
+    default: return launch_fbm_one<R, K, kCfgMixed>(a, grid, smem, st);
+  }
+}
+
+template <typename R, int K>
+size_t fb_mitm_smem() { return MISmem<R, K>::bytes(); }
+
+#define LHMM_INST_FB(R, K)                                                                   \
   template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \
-                                             cudaStream_t);                                  \
+                                             cudaStream_t);
+#define LHMM_INST_VIT(R, K)                                                                  \
   template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
                                               cudaStream_t);
+#define LHMM_INST_FBM(R, K)                                                                  \
+  template cudaError_t launch_fb_mitm<R, K>(const FBMArgs&, int, dim3, size_t, cudaStream_t); \
+  template size_t fb_mitm_smem<R, K>();
 
 #define LHMM_EXTERN_INST(R, K)                                                                      \
   extern template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \
                                                     cudaStream_t);                                  \
   extern template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
-                                                     cudaStream_t);
+                                                     cudaStream_t);                                 \
+  extern template cudaError_t launch_fb_mitm<R, K>(const FBMArgs&, int, dim3, size_t, cudaStream_t); \
+  extern template size_t fb_mitm_smem<R, K>();
 
 }  // namespace lhmm

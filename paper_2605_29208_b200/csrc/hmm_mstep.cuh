@@ -139,6 +139,25 @@ __device__ inline double gamma_newton(double c, double x0, bool& ok) {
   return x;
 }
 
+// fit_gamma_nr (distributions.py:764-786) from exact moments; returns status.
+__device__ inline int32_t gamma_fit(double n, double mean, double var, double sumlog,
+                                    loghmm_emission_t& e) {
+  if (var <= 0.0) return LOGHMM_MS_ERR_GAMMA_VAR;
+  const double c = log(mean) - sumlog / n;
+  if (c <= 0.0) return LOGHMM_MS_ERR_GAMMA_GAP;
+  const double seed = mean * mean / var;
+  bool ok = false;
+  double alpha = gamma_newton(c, seed, ok);
+  int32_t st = LOGHMM_MS_UPDATED;
+  if (!ok) {
+    st |= LOGHMM_MS_WARN_NEWTON;
+    alpha = seed;
+  }
+  e.p[0] = alpha;
+  e.p[1] = alpha / mean;
+  return st;
+}
+
 // Student-t nu objective / score / curvature (distributions.py:995-1009).
 __device__ inline double st_obj(double nu, double n, double mix) {
   return n * (nu / 2.0 * log(nu / 2.0) - lgamma(nu / 2.0)) + nu / 2.0 * mix;
@@ -171,12 +190,19 @@ __global__ void __launch_bounds__(256) reduce_stats_kernel(const double* __restr
 }
 
 // guard_state layout per (stream, state): [mu, sigma, nu0, nu_cand, n, active, k_next, pad]
-constexpr int kGuardStride = 8;
+// guard_state per (stream, state), 16 doubles:
+//  [0..7]  Student-t guard: mu, sigma, nu0, nu_cand, n, active, k_next, -
+//  [8]     variance pass requested (1.0) / not (0.0)
+//  [9]     centre of the second pass (the new mean / location)
+//  [10..12] Student-t old parameters (mu0, sigma0, nu0) for the weights u
+//  [13]    n (total weight),  [14] sum w log y (gamma),  [15] old shape (gamma)
+constexpr int kGuardStride = 16;
 
 __global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const double* __restrict__ tot,
                              int64_t nseq, double eps, double nu_ceiling, double nu_tol,
                              int max_newton, loghmm_model_t* __restrict__ mout,
-                             int32_t* __restrict__ status, double* __restrict__ guard) {
+                             int32_t* __restrict__ status, double* __restrict__ guard,
+                             double var_ratio) {
   const int K = min_->K;
   const int S = min_->n_streams;
   const int tid = threadIdx.x;
@@ -226,6 +252,7 @@ __global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const doub
     int32_t st = LOGHMM_MS_UPDATED;
     double* gs = guard + (size_t)(s * K + j) * kGuardStride;
     gs[5] = 0.0;
+    gs[8] = 0.0;
     if (e.family == LOGHMM_FAM_NONE) {
       // nothing
     } else if (n_state < eps) {
@@ -239,6 +266,13 @@ __global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const doub
           if (var < 0.0) var = 0.0;
           e.p[0] = e.p[0] + d;
           e.p[1] = fmax(sqrt(var), kScaleFloor);
+          // one-pass shifted sums lose ~(d^2/var) relative precision: ask for
+          // the exact two-pass sum (distributions.py:616-620) when large
+          if (!(var > 0.0) || d * d > var_ratio * var) {
+            gs[8] = 1.0;
+            gs[9] = e.p[0];
+            gs[13] = n;
+          }
           break;
         }
         case LOGHMM_FAM_POISSON: {
@@ -258,8 +292,16 @@ __global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const doub
           const double d = q[1] / n;
           const double mean = m_old + d;
           const double var = (q[2] - q[1] * d) / n;
-          if (var <= 0.0) {
+          if (var <= 0.0 && !(d * d > 0.0)) {
             st = LOGHMM_MS_ERR_GAMMA_VAR;
+            break;
+          }
+          if (d * d > var_ratio * var) {
+            // defer the whole fit to the exact second pass
+            gs[8] = 1.0;
+            gs[9] = mean;
+            gs[13] = n;
+            gs[14] = q[3];
             break;
           }
           const double c = log(mean) - q[3] / n;
@@ -331,6 +373,14 @@ __global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const doub
           double s2 = (q[3] - q[2] * dmu) / n;
           if (s2 < 0.0) s2 = 0.0;
           const double sigma = fmax(sqrt(s2), kScaleFloor);
+          if (!(s2 > 0.0) || dmu * dmu * swu > var_ratio * s2 * n) {
+            gs[8] = 1.0;
+            gs[9] = mu;
+            gs[10] = mu0;
+            gs[11] = e.p[1];
+            gs[12] = nu0;
+            gs[13] = n;
+          }
           const double half = (nu0 + 1.0) / 2.0;
           const double mix = q[4] + n * (sp_digamma(half) - log(half));
           double nu = nu0;
@@ -481,6 +531,77 @@ __global__ void guard_select_kernel(loghmm_model_t* __restrict__ mout, int K, in
   e.p[1] = sigma;
   em_constants(e);
   status[sidx * K + j] &= ~LOGHMM_MS_STUDENT_GUARD;
+}
+
+// Exact second pass for flagged states (distributions.py:616-620 two-pass
+// variance; :1051 sigma^2 = sum w u (y - mu)^2 / n): per-block partial sums of
+// w (y - centre)^2 (Gaussian, Gamma) or w u (y - centre)^2 with u at the old
+// Student-t parameters.  Blocks skip states that are not flagged.
+template <typename R>
+__global__ void __launch_bounds__(256) variance_pass_kernel(const R* __restrict__ y,
+                                                            const R* __restrict__ gamma, int64_t N,
+                                                            int K, int sidx,
+                                                            const loghmm_model_t* __restrict__ mout,
+                                                            const double* __restrict__ guard,
+                                                            double* __restrict__ part) {
+  __shared__ double red[256];
+  for (int j = 0; j < K; ++j) {
+    const double* gs = guard + (size_t)(sidx * K + j) * kGuardStride;
+    if (gs[8] == 0.0) continue;
+    const int fam = mout->em[sidx][j].family;
+    const double c = gs[9];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const double w = (double)gamma[i * K + j];
+      if (w > 0.0) {
+        const double yy = (double)y[i];
+        const double d = yy - c;
+        double ww = w;
+        if (fam == LOGHMM_FAM_STUDENT_T) {
+          const double z = (yy - gs[10]) / gs[11];
+          ww = w * ((gs[12] + 1.0) / (gs[12] + z * z));
+        }
+        acc += ww * d * d;
+      }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) part[(size_t)blockIdx.x * K + j] = red[0];
+    __syncthreads();
+  }
+}
+
+__global__ void variance_finish_kernel(loghmm_model_t* __restrict__ mout, int K, int sidx,
+                                       const double* __restrict__ guard,
+                                       const double* __restrict__ part, int nblocks,
+                                       int32_t* __restrict__ status) {
+  const int j = threadIdx.x;
+  if (j >= K) return;
+  const double* gs = guard + (size_t)(sidx * K + j) * kGuardStride;
+  if (gs[8] == 0.0) return;
+  double S = 0.0;
+  for (int blk = 0; blk < nblocks; ++blk) S += part[(size_t)blk * K + j];
+  loghmm_emission_t& e = mout->em[sidx][j];
+  const double n = gs[13];
+  int32_t& st = status[sidx * K + j];
+  if (e.family == LOGHMM_FAM_GAUSSIAN) {
+    e.p[0] = gs[9];
+    e.p[1] = fmax(sqrt(S / n), kScaleFloor);
+  } else if (e.family == LOGHMM_FAM_GAMMA) {
+    st = gamma_fit(n, gs[9], S / n, gs[14], e);
+    if (st >= 16) return;
+  } else if (e.family == LOGHMM_FAM_STUDENT_T) {
+    const double sigma = fmax(sqrt(S / n), kScaleFloor);
+    e.p[1] = sigma;
+    // the guard pass reads sigma from its own scratch
+    const_cast<double*>(gs)[1] = sigma;
+  }
+  em_constants(e);
 }
 
 }  // namespace lhmm

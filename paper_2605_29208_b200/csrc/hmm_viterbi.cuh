@@ -155,10 +155,9 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
   // One recursion step: every lane executes it (no divergence around the
   // shuffles / ballots); lanes past their sequence end keep their score.
   // Lane 0 stores the step's bit-planes (one shared-memory store per step).
-  uint32_t* pl_st = planes;
-  auto step = [&](int t, R yv0, R yv1) {
-    R lb = em0.eval(yv0, lut, lut_n, oob);
-    if (two) lb = N::add(lb, em1.eval(yv1, lut, lut_n, oob));
+  // The emission terms of a block of U steps are evaluated up front so the
+  // loop-carried chain (shuffle -> add -> argmax -> add) runs back to back.
+  auto step = [&](int t, R lb) {
     R cand[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) cand[i] = N::add(__shfl_sync(kFull, delta, g * K + i), la[i]);
@@ -171,18 +170,23 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
     for (int p = 0; p < NP; ++p) w[p] = __ballot_sync(kFull, (bi >> p) & 1);
     if (lane == 0) {
       if constexpr (NP == 1) {
-        pl_st[(size_t)t] = w[0];
+        planes[(size_t)t] = w[0];
       } else if constexpr (NP == 2) {
-        *reinterpret_cast<uint2*>(pl_st + (size_t)t * 2) = make_uint2(w[0], w[1]);
+        *reinterpret_cast<uint2*>(planes + (size_t)t * 2) = make_uint2(w[0], w[1]);
       } else if constexpr (NP == 3) {
 #pragma unroll
-        for (int p = 0; p < 3; ++p) pl_st[(size_t)t * 3 + p] = w[p];
+        for (int p = 0; p < 3; ++p) planes[(size_t)t * 3 + p] = w[p];
       }
     }
   };
+  auto emis = [&](R yv0, R yv1) -> R {
+    R lb = em0.eval(yv0, lut, lut_n, oob);
+    if (two) lb = N::add(lb, em1.eval(yv1, lut, lut_n, oob));
+    return lb;
+  };
 
   constexpr int U = 8;
-  R y0c[U], y0n[U], y1c[U], y1n[U];
+  R y0n[U], y1n[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int tt = min(1 + u, Tlast);
@@ -192,11 +196,9 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
   int t = 1;
 #pragma unroll 1
   for (; t + U <= Tmax; t += U) {
+    R lbs[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      y0c[u] = y0n[u];
-      y1c[u] = y1n[u];
-    }
+    for (int u = 0; u < U; ++u) lbs[u] = emis(y0n[u], y1n[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int tt = min(t + U + u, Tlast);
@@ -204,12 +206,12 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
       y1n[u] = two ? y1g[tt] : R(0);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) step(t + u, y0c[u], y1c[u]);
+    for (int u = 0; u < U; ++u) step(t + u, lbs[u]);
   }
 #pragma unroll 1
   for (; t < Tmax; ++t) {
     const int tt = min(t, Tlast);
-    step(t, y0g[tt], two ? y1g[tt] : R(0));
+    step(t, emis(y0g[tt], two ? y1g[tt] : R(0)));
   }
 
   __syncwarp();

@@ -1,0 +1,5 @@
+// Explicit instantiation: FB kernels for dtype float, K=6.
+#include "hmm_launch.cuh"
+namespace lhmm {
+LHMM_INST_FB(float, 6)
+}

@@ -1,0 +1,5 @@
+// Explicit instantiation: FBM kernels for dtype float, K=6.
+#include "hmm_launch.cuh"
+namespace lhmm {
+LHMM_INST_FBM(float, 6)
+}

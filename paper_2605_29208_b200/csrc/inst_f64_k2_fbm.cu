@@ -1,0 +1,5 @@
+// Explicit instantiation: FBM kernels for dtype double, K=2.
+#include "hmm_launch.cuh"
+namespace lhmm {
+LHMM_INST_FBM(double, 2)
+}

@@ -354,15 +354,40 @@ def reduce_stats(partials: torch.Tensor, ll: torch.Tensor, out: torch.Tensor | N
     return out
 
 
+GUARD_STRIDE = 16  # doubles of scratch per (stream, state)
+
+
+def var_ratio(td: torch.dtype) -> float:
+    """Second-pass trigger for variance-type statistics: (mean shift)^2 / var
+    above which the one-pass shifted sum would lose more than ~1e-11 (fp64)
+    or ~1e-6 (fp32 lane partials) relative precision."""
+    return 1e3 if td == torch.float64 else 10.0
+
+
 def mstep(dm_in: DeviceModel, totals: torch.Tensor, n_sequences: int, config,
-          dm_out: DeviceModel, status: torch.Tensor, guard: torch.Tensor) -> None:
+          dm_out: DeviceModel, status: torch.Tensor, guard: torch.Tensor,
+          td: torch.dtype = torch.float64) -> None:
     L = lib()
     e = config.ecme
     check(
         L.loghmm_mstep(dm_in.ptr(), _ptr(totals), n_sequences, float(config.collapse_epsilon),
-                       float(e.nu_ceiling), float(e.nu_tol), int(e.max_newton), dm_out.ptr(),
-                       _ptr(status), _ptr(guard), _stream()),
+                       float(e.nu_ceiling), float(e.nu_tol), int(e.max_newton), var_ratio(td),
+                       dm_out.ptr(), _ptr(status), _ptr(guard), _stream()),
         "loghmm_mstep",
+    )
+
+
+def variance_pass(batch: Batch, dm_out: DeviceModel, gamma: torch.Tensor, stream_index: int,
+                  guard: torch.Tensor, status: torch.Tensor) -> None:
+    L = lib()
+    K = dm_out.K
+    y = batch.y0 if stream_index == 0 else batch.y1
+    need = int(L.loghmm_guard_workspace_bytes(K, batch.N))
+    wptr, wlen = _WS_GUARD.get(need, y.device)
+    check(
+        L.loghmm_variance_pass(_code(batch.dtype), dm_out.ptr(), _ptr(y), _ptr(gamma), batch.N, K,
+                               stream_index, _ptr(guard), _ptr(status), wptr, wlen, _stream()),
+        "loghmm_variance_pass",
     )
 
 

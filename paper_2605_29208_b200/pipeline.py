@@ -63,7 +63,7 @@ class Pipeline:
         )
         self.totals = torch.empty(width + 1, dtype=torch.float64, device=dev)
         self.status = torch.zeros(self.ns * K, dtype=torch.int32, device=dev)
-        self.guard = torch.zeros(self.ns * K * 8, dtype=torch.float64, device=dev)
+        self.guard = torch.zeros(self.ns * K * engine.GUARD_STRIDE, dtype=torch.float64, device=dev)
         self.need_more = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ws_fb = engine.Workspace()
         self.ws_vit = engine.Workspace()
@@ -72,13 +72,17 @@ class Pipeline:
         fams = self.dm.host["em"]["family"]
         self.student_streams = sorted({s for s in range(self.ns) for j in range(K)
                                        if int(fams[s, j]) == _native.FAM["student_t"]})
+        var_fams = (_native.FAM["gaussian"], _native.FAM["gamma"], _native.FAM["student_t"])
+        self.var_streams = [s for s in range(self.ns)
+                            if any(int(fams[s, j]) in var_fams for j in range(K))]
         # per-kernel CUDA events (recorded on the stream each kernel runs on)
         self.ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for k in ("fb", "vit")}
 
     @property
     def kernels_per_run(self) -> int:
-        return self.KERNELS_PER_RUN + len(self.student_streams)
+        # + variance pass & finish per variance stream, + guard & select per Student-t stream
+        return self.KERNELS_PER_RUN + 2 * len(self.var_streams) + 2 * len(self.student_streams)
 
     def load(self, y) -> None:
         """Copy observations [B, T] (or [B, T, 2]) into the device batch."""
@@ -113,7 +117,9 @@ class Pipeline:
 
             dist.all_reduce(self.totals, group=self.pg)
         engine.mstep(self.dm, self.totals, self.B * (1 if self.pg is None else self._world()),
-                     self.config, self.dm_next, self.status, self.guard)
+                     self.config, self.dm_next, self.status, self.guard, self.td)
+        for s in self.var_streams:
+            engine.variance_pass(self.batch, self.dm_next, self.fb.gamma, s, self.guard, self.status)
         for s in self.student_streams:
             engine.student_guard(self.batch, self.dm_next, self.fb.gamma, s, 2, self.guard,
                                  self.status, self.need_more)

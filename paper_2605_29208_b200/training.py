@@ -166,12 +166,16 @@ def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtyp
     fams = [[int(dm_cur.host["em"][s, j]["family"]) for j in range(K)] for s in range(ns)]
     student = [(s, j) for s in range(ns) for j in range(K) if fams[s][j] == _native.FAM["student_t"]]
     student_streams = sorted({s for s, _ in student})
+    var_fams = (_native.FAM["gaussian"], _native.FAM["gamma"], _native.FAM["student_t"])
+    var_streams = [s for s in range(ns) if any(f in var_fams for f in fams[s])]
     dev = batch.y0.device
-    out = engine.forward_backward(batch, dm_cur, alpha=False, beta=False, gamma=bool(student),
+    # gamma is materialised for the exact second passes (variance, ECME guard)
+    need_gamma = bool(student) or bool(var_streams)
+    out = engine.forward_backward(batch, dm_cur, alpha=False, beta=False, gamma=need_gamma,
                                   stats=True)
     totals = torch.empty(out.partials.shape[1] + 1, dtype=torch.float64, device=dev)
     status = torch.zeros(ns * K, dtype=torch.int32, device=dev)
-    guard = torch.zeros(ns * K * 8, dtype=torch.float64, device=dev)
+    guard = torch.zeros(ns * K * engine.GUARD_STRIDE, dtype=torch.float64, device=dev)
     need_more = torch.zeros(1, dtype=torch.int32, device=dev)
 
     trace: list[float] = []
@@ -180,7 +184,7 @@ def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtyp
     n_msteps = 0
     for iteration in range(1, config.max_iterations + 1):
         if iteration > 1:
-            engine.forward_backward(batch, dm_cur, alpha=False, beta=False, gamma=bool(student),
+            engine.forward_backward(batch, dm_cur, alpha=False, beta=False, gamma=need_gamma,
                                     stats=True, out=out)
         engine.reduce_stats(out.partials, out.ll, totals)
         flags = out.flags.cpu().numpy()
@@ -195,7 +199,9 @@ def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtyp
                 break
         if iteration == config.max_iterations:
             break
-        engine.mstep(dm_cur, totals, batch.B, config, dm_next, status, guard)
+        engine.mstep(dm_cur, totals, batch.B, config, dm_next, status, guard, batch.dtype)
+        for s in var_streams:
+            engine.variance_pass(batch, dm_next, out.gamma, s, guard, status)
         for s in student_streams:
             ncand = 2
             while True:

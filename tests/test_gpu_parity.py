@@ -175,9 +175,16 @@ def test_fp64_viterbi_poisson_bitexact(K):
         assert out.log_joint.cpu().numpy()[b] == j
 
 
+@pytest.fixture(params=["chunked", "mitm"])
+def fb_algo(request, monkeypatch):
+    """Run a test under both forward-backward decompositions."""
+    monkeypatch.setenv("LOGHMM_FB_ALGO", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 6, 8])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
-def test_posteriors_batch_ragged(K, dtype):
+def test_posteriors_batch_ragged(K, dtype, fb_algo):
     rng = np.random.default_rng(11 * K)
     m = _random_gauss_model(rng, K)
     lens = [1, 2, 5, 31, 32, 33, 100, 1000, 1025]
@@ -208,7 +215,7 @@ def test_posteriors_batch_ragged(K, dtype):
             np.testing.assert_allclose(X_[xs], o["xi"], atol=1e-5)
 
 
-def test_baum_welch_matches_reference(golden):
+def test_baum_welch_matches_reference(golden, fb_algo):
     v = golden["vec"]
     for c in golden["cases"]:
         m = to_model(c["pi"], c["A"], c["emissions"])
@@ -347,7 +354,7 @@ def test_config2_full_size(dtype):
 
 @pytest.mark.parametrize("name,B,T,iters", [("c2", 48, 1024, 3), ("c3", 16, 2048, 3),
                                             ("c4", 12, 2000, 3), ("c5", 2, 4096, 2)])
-def test_config_baum_welch_subset(name, B, T, iters):
+def test_config_baum_welch_subset(name, B, T, iters, fb_algo):
     """Baum-Welch parity on a seeded subset of each BASELINE config."""
     cfg = make_config(name, B=B, T=T)
     data = [cfg.data[b] for b in range(B)]
