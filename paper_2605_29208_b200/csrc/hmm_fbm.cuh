@@ -49,6 +49,20 @@ struct FBMArgs {
   int64_t stats_width;
 };
 
+// Asynchronous global->shared copies (LDGSTS) with zero-fill when !pred.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int n = pred ? BYTES : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(gsrc), "n"(BYTES),
+               "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void l2_discard(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
@@ -171,13 +185,14 @@ struct MITraits {
 template <typename R, int K>
 struct MISmem {
   typedef MITraits<R, K> M;
-  static constexpr int YW = 32;                     // y staging depth (steps)
-  static constexpr int YP = M::G + 1;               // y row pitch (odd in 4/8 B units)
+  static constexpr int D = 16;                      // prefetch depth (steps)
+  static constexpr int YR = D * kWarp * 2;          // y ring: [D][lane] x 2 streams
+  static constexpr int WR = D * kWarp * M::KL;      // workspace ring: [D][lane][KL]
   static constexpr int ROW = kMSlab * K;            // staged elements per sequence row
   static constexpr int RP = ROW + (16 / (int)sizeof(R));  // padded row pitch (16 B aligned)
   static constexpr int STG = M::G * RP;             // one staging array
-  // fwd: y0,y1, stage log_alpha, stage gamma ; bwd: y0,y1, stage log_beta, stage gamma
-  static constexpr int PER_WARP = 2 * YW * YP + 2 * STG;
+  // per warp: y ring, workspace ring, stage log_alpha|log_beta, stage gamma
+  static constexpr int PER_WARP = YR + WR + 2 * STG;
   static constexpr int XI = M::G * K * K;           // xi exchange (fwd -> bwd)
   static constexpr size_t bytes() { return (size_t)(2 * PER_WARP + XI) * sizeof(R) + 16; }
 };
@@ -188,10 +203,13 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
   typedef MITraits<R, K> M;
   typedef MISmem<R, K> SM;
   typedef CfgTraits<CFG> TR;
-  constexpr int S = M::S, KL = M::KL, KP = M::KP, G = M::G;
+  constexpr int S = M::S, KL = M::KL, KP = M::KP, G = M::G, D = SM::D;
   constexpr R kL2E = R(1.4426950408889634);
   constexpr R kLN2 = R(0.6931471805599453);
   constexpr double kLN2d = 0.6931471805599453094;
+  // vector stores of a lane's KL states into a [step][K] row are aligned only
+  // when K is a multiple of KL (K = 2, 4, 8)
+  constexpr bool kVecRow = (K % KL) == 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
 
   const int warp = threadIdx.x >> 5;  // 0 forward, 1 backward
@@ -207,9 +225,9 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
 
   R* sm = reinterpret_cast<R*>(smem_raw);
   R* wsm = sm + warp * SM::PER_WARP;
-  R* ys0 = wsm;
-  R* ys1 = ys0 + SM::YW * SM::YP;
-  R* stO = ys1 + SM::YW * SM::YP;  // log_alpha (fwd) / log_beta (bwd)
+  R* yring = wsm;                  // [D][32][2]
+  R* wring = yring + SM::YR;       // [D][32][KL]
+  R* stO = wring + SM::WR;         // log_alpha (fwd) / log_beta (bwd)
   R* stG = stO + SM::STG;          // gamma
   R* xis = sm + 2 * SM::PER_WARP;  // xi exchange [G][K][K]
   __shared__ int s_T[G];
@@ -219,7 +237,6 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
     s_start[q] = start;
   }
 
-  // warp-uniform lengths
   int Tmax = T;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) Tmax = max(Tmax, __shfl_xor_sync(kFull, Tmax, o));
@@ -229,19 +246,20 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
   const R* __restrict__ y1g = two ? reinterpret_cast<const R*>(a.y1) : y0g;
 
   // ---- model -------------------------------------------------------------
+  // State order inside a lane: own states first (perm(i) = j0 + i for i < KL,
+  // then the partner's), so the exchanged half lands at static indices.
+  auto perm = [&](int i) -> int { return i < KL ? j0 + i : (S == 2 ? (1 - h) * KL + (i - KL) : i); };
   const loghmm_model_t* __restrict__ md = a.model;
-  // forward: p_j = sum_i a_i A_ij for own j  -> column block Acol[i][jl] = A[i][j0+jl]
-  // backward: q_i = sum_j A_ij w_j for own i -> row block    Arow[il][j] = A[j0+il][j]
-  R Am[KP][KL];  // fwd: Am[i][jl] = A[i][j0+jl]; bwd: Am[j][il] = A[j0+il][j]
+  R Am[KP][KL];  // fwd: Am[i][l] = A[perm i][j0+l]; bwd: Am[j][l] = A[j0+l][perm j]
   R minA = R(1);
 #pragma unroll
   for (int i = 0; i < KP; ++i)
 #pragma unroll
     for (int l = 0; l < KL; ++l) {
-      const int r = fwd ? i : j0 + l;
-      const int c = fwd ? j0 + l : i;
-      const R v = (r < K && c < K) ? (R)md->A[r * K + c] : R(0);
-      Am[i][l] = v;
+      const int pi_ = perm(i);
+      const int r = fwd ? pi_ : j0 + l;
+      const int c = fwd ? j0 + l : pi_;
+      Am[i][l] = (r < K && c < K) ? (R)md->A[r * K + c] : R(0);
     }
   for (int i = 0; i < K * K; ++i) {
     const R v = (R)md->A[i];
@@ -269,61 +287,33 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
   }
 
   R* __restrict__ W = reinterpret_cast<R*>(a.ws);
-  const int64_t wcol = (int64_t)(blockIdx.x * G + q) * KP + j0;  // element offset in a t row
+  const int64_t wcol = (int64_t)(blockIdx.x * G + q) * KP + j0;
+  const int64_t wstride = a.ws_bstride;
+  const bool wdisc = (h == 0) && (((wcol * (int64_t)sizeof(R)) & 127) == 0);
+  const int dir = fwd ? 1 : -1;
 
-  // y staging: window [yw, yw+YW) of steps for the G sequences, [step][seq]
-  auto stage_y = [&](int yw) {
-    __syncwarp();
-    for (int e = lane; e < SM::YW * G; e += kWarp) {
-      const int qq = e / SM::YW, st = e % SM::YW;  // consecutive lanes: consecutive steps
-      const int t = yw + st;
-      const int Tq = s_T[qq];
-      const int64_t sq = s_start[qq];
-      R v0 = R(0), v1 = R(0);
-      if (t >= 0 && t < Tq) {
-        v0 = y0g[sq + t];
-        if (two) v1 = y1g[sq + t];
-      }
-      ys0[st * SM::YP + qq] = v0;
-      if (two) ys1[st * SM::YP + qq] = v1;
-    }
-    __syncwarp();
-  };
-  // output flush for window [tw, tw+kMSlab): row qq is contiguous in global;
-  // only steps in [lo, hi) of the window were produced by this warp.
-  auto flush = [&](R* __restrict__ out, const R* __restrict__ stg, int tw, int lo, int hi) {
-    __syncwarp();
-    if (out) {
-      constexpr int EPV = 16 / (int)sizeof(R);
-      constexpr int VPR = (SM::ROW + EPV - 1) / EPV;
-      const int s0 = lo > tw ? lo - tw : 0;
-      for (int v = lane; v < G * VPR; v += kWarp) {
-        const int qq = v / VPR, vi = v % VPR;
-        const int Tq = s_T[qq];
-        int s1 = min(hi, Tq) - tw;
-        s1 = s1 < 0 ? 0 : (s1 > kMSlab ? kMSlab : s1);
-        int e0 = vi * EPV, e1 = e0 + EPV;
-        e0 = max(e0, s0 * K);
-        e1 = min(e1, s1 * K);
-        if (e1 <= e0) continue;
-        R* dst = out + (s_start[qq] + tw) * K + e0;
-        const R* src = stg + qq * SM::RP + e0;
-        const bool al = ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (e1 - e0 == EPV);
-        if (al) {
-          *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
-        } else {
-          for (int e2 = 0; e2 < e1 - e0; ++e2) dst[e2] = src[e2];
-        }
-      }
-    }
-    __syncwarp();
-  };
+  // per-lane ring slots: slot(i) = ring + ((i & (D-1)) * 32 + lane) * width
+  R* yslot0 = yring + lane * 2;
+  R* wslot0 = wring + lane * KL;
+  // stage row of this lane: q * RP + step * K + j0
+  R* stOq = stO + q * SM::RP + j0;
+  R* stGq = stG + q * SM::RP + j0;
+
+  // Flush plan: vector v = lane + 32k covers row v / VPR, unit v % VPR.
+  constexpr int EPV = 16 / (int)sizeof(R);
+  constexpr int VPR = (SM::ROW + EPV - 1) / EPV;
+  constexpr int NIT = (G * VPR + kWarp - 1) / kWarp;
+  int f_row[NIT], f_e0[NIT];
+#pragma unroll
+  for (int k = 0; k < NIT; ++k) {
+    const int v = lane + kWarp * k;
+    f_row[k] = v < G * VPR ? v / VPR : -1;
+    f_e0[k] = (v % VPR) * EPV;
+  }
 
   bool oob = false, nan_seen = false;
   int dead_t = INT_MAX;
-
-  // accumulators (own states)
-  R X[KP][KL];  // fwd: X[i][jl] (column block), bwd: X[jl... stored as X[j][il] (row block)
+  R X[KP][KL];
   R gtot[KL], g0[KL];
   R st[TR::S][KL][LOGHMM_NSLOT];
 #pragma unroll
@@ -333,9 +323,9 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
 #pragma unroll
     for (int i = 0; i < KP; ++i) X[i][l] = R(0);
 #pragma unroll
-    for (int s = 0; s < TR::S; ++s)
+    for (int s2 = 0; s2 < TR::S; ++s2)
 #pragma unroll
-      for (int k = 0; k < LOGHMM_NSLOT; ++k) st[s][l][k] = R(0);
+      for (int k = 0; k < LOGHMM_NSLOT; ++k) st[s2][l][k] = R(0);
   }
   __syncthreads();  // s_T / s_start visible
 
@@ -344,13 +334,45 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
   R* __restrict__ outX = reinterpret_cast<R*>(a.xi);
   double LL = 0.0;
 
-  // exchange of the partner's half of a KL-vector (S == 2)
-  auto gather = [&](const R (&own)[KL], R (&full)[KP]) {
+  // window [tw, tw+kMSlab) flush; steps [lo, hi) of it were produced here
+  auto flush = [&](R* __restrict__ out, const R* __restrict__ stg, int tw, int lo, int hi) {
+    __syncwarp();
+    if (out) {
+      const int s0 = lo > tw ? lo - tw : 0;
+#pragma unroll
+      for (int k = 0; k < NIT; ++k) {
+        const int qq = f_row[k];
+        if (qq < 0) continue;
+        int s1 = min(hi, s_T[qq]) - tw;
+        s1 = s1 < 0 ? 0 : (s1 > kMSlab ? kMSlab : s1);
+        const int e0 = max(f_e0[k], s0 * K);
+        const int e1 = min(f_e0[k] + EPV, s1 * K);
+        if (e1 <= e0) continue;
+        R* dst = out + (s_start[qq] + tw) * K + e0;
+        const R* src = stg + qq * SM::RP + e0;
+        if (e1 - e0 == EPV && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
+        } else {
+          for (int e2 = 0; e2 < e1 - e0; ++e2) dst[e2] = src[e2];
+        }
+      }
+    }
+    __syncwarp();
+  };
+  auto st_row = [&](R* p, const R (&v)[KL]) {
+    if constexpr (kVecRow) {
+      LVec<R, KL>::st(p, v);
+    } else {
+#pragma unroll
+      for (int l = 0; l < KL; ++l)
+        if (j0 + l < K) p[l] = v[l];
+    }
+  };
+  auto gother = [&](const R (&own)[KL], R (&full)[KP]) {
 #pragma unroll
     for (int l = 0; l < KL; ++l) {
-      const R o = (S == 2) ? __shfl_xor_sync(kFull, own[l], 1) : R(0);
-      full[h * KL + l] = own[l];
-      if (S == 2) full[(1 - h) * KL + l] = o;
+      full[l] = own[l];
+      if (S == 2) full[KL + l] = __shfl_xor_sync(kFull, own[l], 1);
     }
   };
   auto gmax = [&](R v) -> R {
@@ -362,20 +384,55 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
     return v;
   };
 
+  // ---- prefetch prologue: y for the first D steps of this sweep ----------
+  // sweep step i handles t = fwd ? i : Tmax-1-i
+  const R* y0p = y0g + start + (fwd ? 0 : (Tmax - 1));  // y pointer of step t(i) for this lane
+  const R* y1p = y1g + start + (fwd ? 0 : (Tmax - 1));
+  auto issue_y = [&](int i, const R* p0, const R* p1) {
+    const int t = fwd ? i : Tmax - 1 - i;
+    const bool ok = i < Tmax && t >= 0 && t < T;
+    R* dst = yslot0 + (i & (D - 1)) * (kWarp * 2);
+    cp_async<sizeof(R)>(dst, ok ? (const void*)p0 : (const void*)y0g, ok);
+    if (two) cp_async<sizeof(R)>(dst + 1, ok ? (const void*)p1 : (const void*)y0g, ok);
+  };
+  auto issue_w = [&](int i, const R* wp) {
+    const int t = fwd ? i : Tmax - 1 - i;
+    const bool ok = i < Tmax && t >= 0 && t < T;
+    R* dst = wslot0 + (i & (D - 1)) * (kWarp * KL);
+    if constexpr (KL * sizeof(R) == 16 || KL * sizeof(R) == 8 || KL * sizeof(R) == 4) {
+      cp_async<KL * sizeof(R)>(dst, ok ? (const void*)wp : (const void*)W, ok);
+    } else {
+#pragma unroll
+      for (int l = 0; l < KL; ++l) cp_async<sizeof(R)>(dst + l, ok ? (const void*)(wp + l) : (const void*)W, ok);
+    }
+  };
+  for (int i = 0; i < D; ++i) {
+    issue_y(i, y0p + dir * i, y1p + dir * i);
+    cp_async_commit();
+  }
+  const int iH = fwd ? H : Tmax - H;  // sweep index of the first combine step
+
   if (fwd) {
     // ===================== forward warp =====================
     R av[KL];  // alpha~ (linear, own states)
     double lam = 0.0;
+    int ncd = nn;
+    const R* wpf = W + (int64_t)H * wstride + wcol;  // W row of the step being prefetched
 #pragma unroll 1
     for (int t = 0; t < Tmax; ++t) {
       if (t == H) {
         __threadfence_block();
         __syncthreads();  // both directions finished their first half
+        for (int i = H; i < H + D; ++i) issue_w(i, W + (int64_t)i * wstride + wcol);
+        wpf = W + (int64_t)(H + D) * wstride + wcol;
+        cp_async_wait_all();
+      } else {
+        cp_async_wait<D - 1>();
       }
-      if ((t % SM::YW) == 0) stage_y(t);
       const bool act = t < T;
-      const R yv0 = ys0[(t % SM::YW) * SM::YP + q];
-      const R yv1 = two ? ys1[(t % SM::YW) * SM::YP + q] : R(0);
+      const R* yr = yslot0 + (t & (D - 1)) * (kWarp * 2);
+      const R yv0 = yr[0];
+      const R yv1 = two ? yr[1] : R(0);
       if (act && (isnan(yv0) || isnan(yv1))) nan_seen = true;
       ObsFeat<R> f0, f1;
       R lb[KL];
@@ -387,11 +444,10 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
       if (act && !(m > N::ninf()) && t < dead_t) dead_t = t;
       const bool fin = m > N::ninf();
       const R m2 = m * kL2E;
-      R o[KL];
-      R g[KL];
+      R o[KL], g[KL];
       bool have_g = false;
       R aprev[KP];
-      gather(av, aprev);
+      gother(av, aprev);
       if (t == 0) {
         R u[KL];
 #pragma unroll
@@ -423,10 +479,7 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
         if (t >= H) {
           // combine with beta~_t: gamma_t and xi_{t-1}
           R bet[KL];
-#pragma unroll
-          for (int l = 0; l < KL; ++l) bet[l] = R(0);
-          const R* wp = W + (int64_t)t * a.ws_bstride + wcol;
-          if (act) LVec<R, KL>::ld(wp, bet);
+          LVec<R, KL>::ld(wslot0 + (t & (D - 1)) * (kWarp * KL), bet);
           R v[KL];
           R Zp = R(0);
 #pragma unroll
@@ -435,31 +488,35 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
             Zp = fma(p[l], v[l], Zp);
           }
           const R iz = N::frcp(gsum(Zp));
-          // single-use workspace line: drop it from L2 once consumed
-          if (act && h == 0 && (((wcol * (int64_t)sizeof(R)) & 127) == 0)) l2_discard(wp);
+          if (act && wdisc) l2_discard(W + (int64_t)t * wstride + wcol);
 #pragma unroll
           for (int l = 0; l < KL; ++l) {
             const R cv = v[l] * iz;
             g[l] = p[l] * cv;
+            if (act) {
 #pragma unroll
-            for (int i = 0; i < KP; ++i) X[i][l] = fma(aprev[i], cv, X[i][l]);
-            if (outX && act) {
+              for (int i = 0; i < KP; ++i) X[i][l] = fma(aprev[i], cv, X[i][l]);
+            }
+            if (outX && act && j0 + l < K) {
               R* xr = outX + ((start - b) + (t - 1)) * (int64_t)(K * K);
-              if (j0 + l < K)
-                for (int i = 0; i < K; ++i) xr[i * K + j0 + l] = aprev[i] * Am[i][l] * cv;
+              for (int i = 0; i < KP; ++i)
+                if (perm(i) < K) xr[perm(i) * K + j0 + l] = aprev[i] * Am[i][l] * cv;
             }
           }
           have_g = act;
         }
+        if (act) {
 #pragma unroll
-        for (int l = 0; l < KL; ++l) av[l] = p[l] * bb[l];
-        lam += fin ? (double)m2 : 0.0;
-        if ((t % nn) == 0) {  // warp-uniform renormalisation schedule
+          for (int l = 0; l < KL; ++l) av[l] = p[l] * bb[l];
+          lam += fin ? (double)m2 : 0.0;
+        }
+        if (--ncd == 0) {  // warp-uniform renormalisation schedule
+          ncd = nn;
           R mx = av[0];
 #pragma unroll
           for (int l = 1; l < KL; ++l) mx = rmax(mx, av[l]);
           mx = gmax(mx);
-          if (mx > R(0)) {
+          if (act && mx > R(0)) {
             int e;
             const R sc = N::pow2_scale(mx, e);
             lam += (double)e;
@@ -468,14 +525,11 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
           }
         }
       }
-      if (t < H && act) {
-        // store alpha~_t for the backward warp
-        LVec<R, KL>::st(W + (int64_t)t * a.ws_bstride + wcol, av);
-      }
+      if (t < H && act) LVec<R, KL>::st(W + (int64_t)t * wstride + wcol, av);
       if (act) {
-        LVec<R, KL>::st(stO + q * SM::RP + (t % kMSlab) * K + j0, o);
+        st_row(stOq + (t & (kMSlab - 1)) * K, o);
         if (have_g) {
-          if (outG) LVec<R, KL>::st(stG + q * SM::RP + (t % kMSlab) * K + j0, g);
+          if (outG) st_row(stGq + (t & (kMSlab - 1)) * K, g);
           em.stats(st, g, f0, f1);
           if (t < T - 1) {
 #pragma unroll
@@ -483,17 +537,24 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
           }
         }
       }
-      if ((t % kMSlab) == kMSlab - 1 || t == Tmax - 1) {
-        const int tw = t - (t % kMSlab);
+      // refill the rings D steps ahead (slot t % D was consumed above)
+      issue_y(t + D, y0p + (t + D), y1p + (t + D));
+      if (t >= H) {
+        issue_w(t + D, wpf);
+        wpf += wstride;
+      }
+      cp_async_commit();
+      if ((t & (kMSlab - 1)) == kMSlab - 1 || t == Tmax - 1) {
+        const int tw = t & ~(kMSlab - 1);
         flush(outO, stO, tw, tw, tw + kMSlab);
         if (tw + kMSlab > H) flush(outG, stG, tw, H, tw + kMSlab);
       }
     }
+    cp_async_wait_all();
     if (H >= Tmax) {
       __threadfence_block();
       __syncthreads();  // matches the backward warp's split barrier
     }
-    // log-likelihood
     R s = R(0);
 #pragma unroll
     for (int l = 0; l < KL; ++l) s += av[l];
@@ -502,22 +563,33 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
     if (T == 0) LL = -CUDART_INF;
   } else {
     // ===================== backward warp =====================
-    R bt[KL];  // beta~_{t+1} (linear, own states)
+    R bt[KL];    // beta~_{t+1} (linear, own states)
     double rho = 0.0;
-    R lbn[KL];   // emission log-density at t+1 (own states), natural units
+    R lbn[KL];   // emission log-density at t+1 (own states)
     R mn = R(0); // its max over all states
     bool finn = true;
-    // iterate t = Tmax-1 .. 0; lane active when t < T
+#pragma unroll
+    for (int l = 0; l < KL; ++l) {
+      bt[l] = R(0);
+      lbn[l] = R(0);
+    }
+    int ncd = nn;
+    const R* wpf = W + (int64_t)(H - 1 - D) * wstride + wcol;
 #pragma unroll 1
     for (int t = Tmax - 1; t >= 0; --t) {
-      if (t == Tmax - 1 || (t % SM::YW) == SM::YW - 1) stage_y(t - (t % SM::YW));
+      const int it = Tmax - 1 - t;
       if (t == H - 1) {
         __threadfence_block();
         __syncthreads();
+        for (int i = iH; i < iH + D; ++i) issue_w(i, W + (int64_t)(Tmax - 1 - i) * wstride + wcol);
+        cp_async_wait_all();
+      } else {
+        cp_async_wait<D - 1>();
       }
       const bool act = t < T;
-      const R yv0 = ys0[(t % SM::YW) * SM::YP + q];
-      const R yv1 = two ? ys1[(t % SM::YW) * SM::YP + q] : R(0);
+      const R* yr = yslot0 + (it & (D - 1)) * (kWarp * 2);
+      const R yv0 = yr[0];
+      const R yv1 = two ? yr[1] : R(0);
       ObsFeat<R> f0, f1;
       R lb[KL];
       em.eval(yv0, yv1, f0, f1, lb, oob);
@@ -525,18 +597,14 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
 #pragma unroll
       for (int l = 1; l < KL; ++l) m = rmax(m, lb[l]);
       m = gmax(m);
-      R o[KL], g[KL];
-      R qv[KL];
+      R o[KL], g[KL], qv[KL];
       bool have_g = false;
       const bool first = (t == T - 1);
-      // recursion beta_t = A (b_{t+1} . beta_{t+1}) for every lane (uniform
-      // shuffles); lanes at their first step take beta_{T-1} = 1 instead.
       R w[KL];
 #pragma unroll
-      for (int l = 0; l < KL; ++l)
-        w[l] = (finn ? N::fex2(fma(lbn[l], kL2E, -mn * kL2E)) : R(0)) * bt[l];
+      for (int l = 0; l < KL; ++l) w[l] = (finn ? N::fex2(fma(lbn[l], kL2E, -mn * kL2E)) : R(0)) * bt[l];
       R wf[KP];
-      gather(w, wf);
+      gother(w, wf);
 #pragma unroll
       for (int l = 0; l < KL; ++l) {
         R acc = Am[0][l] * wf[0];
@@ -544,11 +612,7 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
         for (int jx = 1; jx < KP; ++jx) acc = fma(Am[jx][l], wf[jx], acc);
         qv[l] = first ? ((j0 + l < K) ? R(1) : R(0)) : acc;
       }
-      if (first) {
-        rho = 0.0;
-      } else {
-        rho += finn ? (double)(mn * kL2E) : 0.0;
-      }
+      if (act) rho = first ? 0.0 : rho + (finn ? (double)(mn * kL2E) : 0.0);
       {
         const R rr = (R)rho;
 #pragma unroll
@@ -557,17 +621,13 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
       if (t < H) {
         // combine with alpha~_t: gamma_t and xi_t (pair t, t+1)
         R al[KL];
-#pragma unroll
-        for (int l = 0; l < KL; ++l) al[l] = R(0);
-        const R* wp = W + (int64_t)t * a.ws_bstride + wcol;
-        if (act) LVec<R, KL>::ld(wp, al);
+        LVec<R, KL>::ld(wslot0 + (it & (D - 1)) * (kWarp * KL), al);
         R Zp = R(0);
 #pragma unroll
         for (int l = 0; l < KL; ++l) Zp = fma(al[l], qv[l], Zp);
         const R iz = N::frcp(gsum(Zp));
-        if (act && h == 0 && (((wcol * (int64_t)sizeof(R)) & 127) == 0)) l2_discard(wp);
-        // the pair (H-1, H) belongs to the forward warp
-        const bool pair = act && !first && t < H - 1;
+        if (act && wdisc) l2_discard(W + (int64_t)t * wstride + wcol);
+        const bool pair = act && !first && t < H - 1;  // (H-1, H) is the forward warp's
 #pragma unroll
         for (int l = 0; l < KL; ++l) {
           g[l] = al[l] * qv[l] * iz;
@@ -577,13 +637,15 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
             for (int jx = 0; jx < KP; ++jx) X[jx][l] = fma(ai, wf[jx], X[jx][l]);
             if (outX && j0 + l < K) {
               R* xr = outX + ((start - b) + t) * (int64_t)(K * K);
-              for (int jx = 0; jx < K; ++jx) xr[(j0 + l) * K + jx] = ai * Am[jx][l] * wf[jx];
+              for (int jx = 0; jx < KP; ++jx)
+                if (perm(jx) < K) xr[(j0 + l) * K + perm(jx)] = ai * Am[jx][l] * wf[jx];
             }
           }
         }
         have_g = act;
       }
-      if ((t % nn) == 0) {  // warp-uniform renormalisation schedule
+      if (--ncd == 0) {  // warp-uniform renormalisation schedule
+        ncd = nn;
         R mx = qv[0];
 #pragma unroll
         for (int l = 1; l < KL; ++l) mx = rmax(mx, qv[l]);
@@ -599,10 +661,10 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
       if (act) {
 #pragma unroll
         for (int l = 0; l < KL; ++l) bt[l] = qv[l];
-        if (t >= H) LVec<R, KL>::st(W + (int64_t)t * a.ws_bstride + wcol, bt);
-        LVec<R, KL>::st(stO + q * SM::RP + (t % kMSlab) * K + j0, o);
+        if (t >= H) LVec<R, KL>::st(W + (int64_t)t * wstride + wcol, bt);
+        st_row(stOq + (t & (kMSlab - 1)) * K, o);
         if (have_g) {
-          if (outG) LVec<R, KL>::st(stG + q * SM::RP + (t % kMSlab) * K + j0, g);
+          if (outG) st_row(stGq + (t & (kMSlab - 1)) * K, g);
           em.stats(st, g, f0, f1);
           if (t < T - 1) {
 #pragma unroll
@@ -613,17 +675,23 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
             for (int l = 0; l < KL; ++l) g0[l] = g[l];
           }
         }
-        // carry emission at t for the next (lower) step
 #pragma unroll
         for (int l = 0; l < KL; ++l) lbn[l] = lb[l];
         mn = m;
         finn = m > N::ninf();
       }
-      if ((t % kMSlab) == 0) {
+      issue_y(it + D, y0p - (it + D), y1p - (it + D));
+      if (t < H) {
+        issue_w(it + D, wpf);
+        wpf -= wstride;
+      }
+      cp_async_commit();
+      if ((t & (kMSlab - 1)) == 0) {
         flush(outO, stO, t, t, t + kMSlab);
         if (t < H) flush(outG, stG, t, t, H);
       }
     }
+    cp_async_wait_all();
   }
 
   // ---- per-sequence results ----------------------------------------------
@@ -634,7 +702,7 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
     for (int i = 0; i < KP; ++i)
 #pragma unroll
       for (int l = 0; l < KL; ++l)
-        if (i < K && j0 + l < K) xq[i * K + j0 + l] = X[i][l];
+        if (perm(i) < K && j0 + l < K) xq[perm(i) * K + j0 + l] = X[i][l];
   }
   __shared__ int s_dead[G];
   __shared__ int s_flag[G];
@@ -691,8 +759,11 @@ __global__ void __launch_bounds__(64) fb_mitm_kernel(const FBMArgs a) {
       for (int l = 0; l < KL; ++l) {
         const int i = j0 + l;
         if (i >= K) continue;
-        for (int jx = 0; jx < K; ++jx)
-          row[i * K + jx] = ((double)X[jx][l] + (double)xq[i * K + jx]) * (double)Am[jx][l];
+        for (int jx = 0; jx < KP; ++jx) {
+          const int j = perm(jx);
+          if (j >= K) continue;
+          row[i * K + j] = ((double)X[jx][l] + (double)xq[i * K + j]) * (double)Am[jx][l];
+        }
       }
 #pragma unroll
       for (int l = 0; l < KL; ++l) {
