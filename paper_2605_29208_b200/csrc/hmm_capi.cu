@@ -76,9 +76,8 @@ static FBGeom fb_geom(int K, int esz, int n_streams, int64_t max_T) {
   // the carve = y_pitch elements so that 32*y_pitch covers it
   g.y_pitch = g.Lmax + (g.Lmax + 31) / 32 + 1;
   const int V = (kb % 16 == 0) ? 16 : (kb % 8 == 0) ? 8 : 4;
-  int aunits = g.Lmax * kb / V;
-  if ((aunits & 1) == 0) aunits += 1;
-  g.a_pitch = aunits * V / esz;
+  (void)V;
+  g.a_pitch = 0;  // beta~ lives in the global (L2-resident) workspace
   int sunits = kSlab * kb / 16;
   if ((sunits & 1) == 0) sunits += 1;
   g.s_pitch = sunits * 16 / esz;
@@ -128,6 +127,30 @@ static cudaError_t dispatch_fb_small(int K, const FBArgs& a, int cfg, bool gl, d
   }
 }
 
+// Two-lane Viterbi (K in [2,4]) geometry: nibble backpointer words in smem.
+static bool vit2_ok(int K, int64_t max_T, int* wpb, size_t* smem, int* warp_words) {
+  if (K < 2 || K > 4) return false;
+  const char* env = getenv("LOGHMM_VIT_ALGO");
+  if (env && strcmp(env, "klane") == 0) return false;
+  const int64_t words = 2 * kWarp * kPathPitch + ((max_T + 7) / 8) * kWarp;
+  const int64_t bytes = ((words + 3) & ~3LL) * 4;
+  if (bytes > 100 * 1024) return false;
+  *warp_words = (int)((words + 3) & ~3LL);
+  *wpb = (int)std::max<int64_t>(1, std::min<int64_t>(4, (200 * 1024) / bytes));
+  *smem = (size_t)bytes * (*wpb);
+  return true;
+}
+
+template <typename R>
+static cudaError_t dispatch_vit2(int K, const VitArgs& a, int cfg, dim3 grid, dim3 block,
+                                 size_t smem, cudaStream_t st) {
+  switch (K) {
+    case 2: return launch_vit2<R, 2>(a, cfg, grid, block, smem, st);
+    case 3: return launch_vit2<R, 3>(a, cfg, grid, block, smem, st);
+    default: return launch_vit2<R, 4>(a, cfg, grid, block, smem, st);
+  }
+}
+
 template <typename R>
 static cudaError_t dispatch_vit_small(int K, const VitArgs& a, int cfg, bool gl, dim3 grid,
                                       dim3 block, size_t smem, cudaStream_t st) {
@@ -145,15 +168,17 @@ static cudaError_t dispatch_vit_small(int K, const VitArgs& a, int cfg, bool gl,
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// Forward-backward decomposition: meet-in-the-middle (hmm_fbm.cuh) when the
-// batch alone fills the GPU, else the chunked scan over T (hmm_fb.cuh).
+// Forward-backward decomposition: chunked scan over T (hmm_fb.cuh) by
+// default; meet-in-the-middle (hmm_fbm.cuh) on request.
 // LOGHMM_FB_ALGO=chunked|mitm forces one (tests exercise both).
 static bool use_mitm(int K, int64_t B) {
   if (K > 8 || K < 2) return false;
   const char* env = getenv("LOGHMM_FB_ALGO");
   if (env && strcmp(env, "chunked") == 0) return false;
   if (env && strcmp(env, "mitm") == 0) return true;
-  return B >= 1024;
+  // the chunked scan is currently faster at every measured shape (see
+  // profiles/); the meet-in-the-middle kernel is kept behind the switch
+  return false;
 }
 
 static int64_t mitm_kp(int K) { return K >= 2 ? 2 * ((K + 1) / 2) : K; }
@@ -196,7 +221,7 @@ size_t loghmm_fb_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N,
     return align256((size_t)max_T * Bp * mitm_kp(K) * esz);
   }
   FBGeom g = fb_geom(K, esz, 2, max_T);
-  return g.global ? align256((size_t)N * K * esz) : 0;
+  return align256((size_t)B * g.Lmax * kWarp * K * esz);
 }
 
 size_t loghmm_viterbi_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N,
@@ -346,7 +371,17 @@ int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm
   a.back = back;
   a.flags = flags;
   cudaError_t e;
-  if (K <= 8) {
+  int v2_wpb = 0, v2_words = 0;
+  size_t v2_smem = 0;
+  if (vit2_ok(K, max_T, &v2_wpb, &v2_smem, &v2_words)) {
+    a.warp_smem_words = v2_words;
+    int fams = 0;
+    const int cfg = cfg_of(h_desc, &fams);
+    const int64_t warps = (B + 15) / 16;
+    dim3 grid((unsigned)((warps + v2_wpb - 1) / v2_wpb)), block(32 * v2_wpb);
+    e = dtype == LOGHMM_F64 ? dispatch_vit2<double>(K, a, cfg, grid, block, v2_smem, st)
+                            : dispatch_vit2<float>(K, a, cfg, grid, block, v2_smem, st);
+  } else if (K <= 8) {
     VitGeom g = vit_geom(K, max_T);
     a.planes_ws = (uint32_t*)workspace;
     a.plane_words = g.plane_words;

@@ -457,8 +457,7 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
   R* wsm = reinterpret_cast<R*>(smem_raw) + (size_t)wib * a.warp_smem_elems;
   R* ybuf0 = wsm;
   R* ybuf1 = ybuf0 + kWarp * a.y_pitch;
-  R* abuf = ybuf1 + (two ? kWarp * a.y_pitch : 0);
-  R* stA = abuf + kWarp * a.a_pitch;
+  R* stA = ybuf1 + (two ? kWarp * a.y_pitch : 0);
   R* stB = stA + kWarp * a.s_pitch;
   if (kGlobal) {
     stA = wsm;
@@ -699,8 +698,14 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
     normalise_vec2<R, K>(b_ex, rho_ex);
   }
 
-  // Row-major base of this warp's beta~ store.
-  R* aw = kGlobal ? reinterpret_cast<R*>(a.alpha_ws) + (start + t0) * K : abuf + lane * a.a_pitch;
+  // beta~ store: global workspace, per sequence [L][32 lanes][K] so every
+  // per-step access of the warp is one contiguous 32*K row.  Written by the
+  // backward re-sweep and read once by the forward re-sweep shortly after, so
+  // it lives in L2; each line is discarded after its read.
+  constexpr int AW_STEP = kWarp * K;
+  R* aw = reinterpret_cast<R*>(a.alpha_ws) + b * (int64_t)a.Lmax * AW_STEP + lane * K;
+  constexpr bool kDisc = (128 % (K * (int)sizeof(R))) == 0;
+  const bool disc_lane = kDisc && (((lane * K * (int)sizeof(R)) & 127) == 0);
   const bool vec_ok = ((start * K * (int64_t)sizeof(R)) % 16 == 0) &&
                       ((L * K * (int)sizeof(R)) % 16 == 0);
   FlushPlan<R, K> fplan;
@@ -721,7 +726,7 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
 #pragma unroll 1
     for (int s = L - 1; s >= 0; --s) {
       if (s == s_top) {
-        VecIO<R, K>::st(aw + s * K, bt);
+        VecIO<R, K>::st(aw + s * AW_STEP, bt);
         if (outB) {
           const R rr = (R)rho;
           R o[K];
@@ -764,7 +769,7 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
           cnt = 0;
           normalise_vec2<R, K>(bt, rho);
         }
-        VecIO<R, K>::st(aw + s * K, bt);
+        VecIO<R, K>::st(aw + s * AW_STEP, bt);
       }
       if ((s % kSlab) == 0 && outB) {
         __syncwarp();
@@ -804,7 +809,8 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
         R lb[K];
         em.eval(yat0(s), yat1(s), f0, f1, lb, oob);
         R bet[K];
-        VecIO<R, K>::ld(aw + s * K, bet);
+        VecIO<R, K>::ld(aw + s * AW_STEP, bet);
+        if (disc_lane) l2_discard(aw + s * AW_STEP);
         R g[K];
         if (t == 0) {
           R u[K];

@@ -5,6 +5,7 @@
 #include "hmm_fb.cuh"
 #include "hmm_fbm.cuh"
 #include "hmm_viterbi.cuh"
+#include "hmm_viterbi2.cuh"
 
 namespace lhmm {
 
@@ -71,6 +72,34 @@ cudaError_t launch_vit_small(const VitArgs& a, int cfg, bool global, dim3 grid, 
 }
 
 template <typename R, int K, int CFG>
+static cudaError_t launch_vit2_one(const VitArgs& a, dim3 grid, dim3 block, size_t smem,
+                                   cudaStream_t st) {
+  if constexpr (K >= 2 && K <= 4) {
+    auto fn = viterbi2_kernel<R, K, CFG>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, block, smem, st>>>(a);
+    return cudaGetLastError();
+  } else {
+    return cudaErrorInvalidValue;
+  }
+}
+
+template <typename R, int K>
+cudaError_t launch_vit2(const VitArgs& a, int cfg, dim3 grid, dim3 block, size_t smem,
+                        cudaStream_t st) {
+  switch (cfg) {
+    case kCfgGauss: return launch_vit2_one<R, K, kCfgGauss>(a, grid, block, smem, st);
+    case kCfgStudent: return launch_vit2_one<R, K, kCfgStudent>(a, grid, block, smem, st);
+    case kCfgGamma: return launch_vit2_one<R, K, kCfgGamma>(a, grid, block, smem, st);
+    case kCfgVonMises: return launch_vit2_one<R, K, kCfgVonMises>(a, grid, block, smem, st);
+    case kCfgPoisson: return launch_vit2_one<R, K, kCfgPoisson>(a, grid, block, smem, st);
+    case kCfgGammaVM: return launch_vit2_one<R, K, kCfgGammaVM>(a, grid, block, smem, st);
+    default: return launch_vit2_one<R, K, kCfgMixed>(a, grid, block, smem, st);
+  }
+}
+
+template <typename R, int K, int CFG>
 static cudaError_t launch_fbm_one(const FBMArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   auto fn = fb_mitm_kernel<R, K, CFG>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -100,7 +129,8 @@ size_t fb_mitm_smem() { return MISmem<R, K>::bytes(); }
                                              cudaStream_t);
 #define LHMM_INST_VIT(R, K)                                                                  \
   template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
-                                              cudaStream_t);
+                                              cudaStream_t);                                 \
+  template cudaError_t launch_vit2<R, K>(const VitArgs&, int, dim3, dim3, size_t, cudaStream_t);
 #define LHMM_INST_FBM(R, K)                                                                  \
   template cudaError_t launch_fb_mitm<R, K>(const FBMArgs&, int, dim3, size_t, cudaStream_t); \
   template size_t fb_mitm_smem<R, K>();
@@ -110,6 +140,7 @@ size_t fb_mitm_smem() { return MISmem<R, K>::bytes(); }
                                                     cudaStream_t);                                  \
   extern template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
                                                      cudaStream_t);                                 \
+  extern template cudaError_t launch_vit2<R, K>(const VitArgs&, int, dim3, dim3, size_t, cudaStream_t); \
   extern template cudaError_t launch_fb_mitm<R, K>(const FBMArgs&, int, dim3, size_t, cudaStream_t); \
   extern template size_t fb_mitm_smem<R, K>();
 

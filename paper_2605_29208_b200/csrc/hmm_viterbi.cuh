@@ -185,25 +185,30 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
     return lb;
   };
 
+  // y prefetched two blocks (2U steps) ahead so DRAM latency stays hidden
   constexpr int U = 8;
-  R y0n[U], y1n[U];
+  R y0a[U], y1a[U], y0b[U], y1b[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const int tt = min(1 + u, Tlast);
-    y0n[u] = y0g[tt];
-    y1n[u] = two ? y1g[tt] : R(0);
+    const int ta = min(1 + u, Tlast), tb2 = min(1 + U + u, Tlast);
+    y0a[u] = y0g[ta];
+    y1a[u] = two ? y1g[ta] : R(0);
+    y0b[u] = y0g[tb2];
+    y1b[u] = two ? y1g[tb2] : R(0);
   }
   int t = 1;
 #pragma unroll 1
   for (; t + U <= Tmax; t += U) {
     R lbs[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) lbs[u] = emis(y0n[u], y1n[u]);
+    for (int u = 0; u < U; ++u) lbs[u] = emis(y0a[u], y1a[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int tt = min(t + U + u, Tlast);
-      y0n[u] = y0g[tt];
-      y1n[u] = two ? y1g[tt] : R(0);
+      y0a[u] = y0b[u];
+      y1a[u] = y1b[u];
+      const int tt = min(t + 2 * U + u, Tlast);
+      y0b[u] = y0g[tt];
+      y1b[u] = two ? y1g[tt] : R(0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) step(t + u, lbs[u]);
@@ -268,15 +273,27 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
     const unsigned gsh = (unsigned)(gg * K);
     // compose the chunk's map: end state (t1-1) -> state at t0-1
     unsigned F = 0x76543210u;
+    {
+      const int tlo = max(t0, 1);
+      constexpr int BB = 8;
 #pragma unroll 1
-    for (int t = t1 - 1; t >= t0 && t >= 1; --t) {
-      unsigned pl[NP > 0 ? NP : 1];
+      for (int tb = t1 - 1; tb >= tlo; tb -= BB) {
+        unsigned plb[BB][NP > 0 ? NP : 1];
 #pragma unroll
-      for (int p = 0; p < NP; ++p) pl[p] = planes[(size_t)t * NP + p] >> gsh;
-      unsigned nf = 0;
+        for (int u = 0; u < BB; ++u) {
+          const int t = tb - u;
 #pragma unroll
-      for (int e = 0; e < K; ++e) nf |= plane_lookup<NP>(pl, nib(F, e)) << (4 * e);
-      F = nf;
+          for (int p = 0; p < NP; ++p) plb[u][p] = t >= tlo ? planes[(size_t)t * NP + p] >> gsh : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < BB; ++u) {
+          if (tb - u < tlo) break;
+          unsigned nf = 0;
+#pragma unroll
+          for (int e = 0; e < K; ++e) nf |= plane_lookup<NP>(plb[u], nib(F, e)) << (4 * e);
+          F = nf;
+        }
+      }
     }
     // inclusive suffix scan: H_c = F_c o F_{c+1} o ... o F_31
     unsigned H = F;
@@ -295,18 +312,28 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
     unsigned cur = nib(Hnext, blast);
     // re-walk the chunk, staging the path in shared memory
     int64_t* out = a.path + sg;
+    // re-walk in windows of kPathSlab steps [w0, w0+8): plane loads of the
+    // window are issued together, then the dependent lookups run back to back
+    const int wtop = ((L - 1) / kPathSlab) * kPathSlab;
 #pragma unroll 1
-    for (int s = L - 1; s >= 0; --s) {
-      const int t = t0 + s;
-      if (t < t1) {
-        pstage[lane * kPathPitch + (s % kPathSlab)] = (int64_t)cur;
-        if (t >= 1) {
-          unsigned pl[NP > 0 ? NP : 1];
+    for (int w0 = wtop; w0 >= 0; w0 -= kPathSlab) {
+      unsigned plc[kPathSlab][NP > 0 ? NP : 1];
 #pragma unroll
-          for (int p = 0; p < NP; ++p) pl[p] = planes[(size_t)t * NP + p] >> gsh;
-          cur = plane_lookup<NP>(pl, cur);
+      for (int u = 0; u < kPathSlab; ++u) {
+        const int tu = t0 + w0 + u;
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+          plc[u][p] = (tu >= 1 && tu < t1) ? planes[(size_t)tu * NP + p] >> gsh : 0u;
+      }
+#pragma unroll
+      for (int u = kPathSlab - 1; u >= 0; --u) {
+        const int tu = t0 + w0 + u;
+        if (w0 + u < L && tu < t1) {
+          pstage[lane * kPathPitch + u] = (int64_t)cur;
+          if (tu >= 1) cur = plane_lookup<NP>(plc[u], cur);
         }
       }
+      const int s = w0;
       if ((s % kPathSlab) == 0) {
         __syncwarp();
         // rows: lane-chunk c covers steps c*L + s .. +kPathSlab within [c*L, min(c*L+L,Tg))

@@ -1,0 +1,273 @@
+// hmm_viterbi2.cuh — batched Viterbi for 2 <= K <= 4, two lanes per sequence.
+//
+// Same contract and operation order as hmm_viterbi.cuh (inference.py:191-210,
+// bit-exact backpointers and path), with a lighter layout for small K:
+// lane (q, h) of a warp owns states j0 = 2h, 2h+1 of sequence q (16 sequences
+// per warp).  Each step the partner's two scores arrive with two shuffles, the
+// lane evaluates the 2 x K candidates and two first-index argmax trees, and
+// appends its two 2-bit backpointers to a nibble accumulator that is stored
+// to shared memory every 8 steps ([t/8][lane] words).
+#pragma once
+
+#include "hmm_viterbi.cuh"
+
+namespace lhmm {
+
+template <typename R, int K, int CFG>
+__global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
+  static_assert(K >= 2 && K <= 4, "two-lane Viterbi covers 2 <= K <= 4");
+  typedef Num<R> N;
+  typedef VitFams<CFG> VF;
+  constexpr int KL = 2;  // states per lane
+  constexpr int G = 16;  // sequences per warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const int q = lane >> 1, h = lane & 1;
+  const int j0 = 2 * h;
+  const int64_t b = warp_id * G + q;
+  const bool valid = b < a.B;
+  if (warp_id * G >= a.B) return;
+
+  uint32_t* wsm = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wib * a.warp_smem_words;
+  int64_t* pstage = reinterpret_cast<int64_t*>(wsm);  // kWarp * kPathPitch int64
+  uint32_t* bpw = kWarp * kPathPitch * 2 + wsm;         // [ceil(Tmax/8)][32] nibble words
+
+  const loghmm_model_t* __restrict__ md = a.model;
+  const int64_t start = valid ? a.offsets[b] : 0;
+  const int T = valid ? (int)(a.offsets[b + 1] - start) : 0;
+  const R* __restrict__ y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const bool two = VF::TWO && a.n_streams > 1;
+  const R* __restrict__ y1g = two ? reinterpret_cast<const R*>(a.y1) + start : y0g;
+
+  // la[i][l] = log A[i][j0 + l] in natural row order i (the argmax scans i
+  // ascending); padded states (>= K) get -inf everywhere.
+  R la[4][KL];
+  ExactEm<R, VF::F0> em0[KL];
+  ExactEm<R, VF::F1> em1[KL];
+  bool padj[KL];
+#pragma unroll
+  for (int l = 0; l < KL; ++l) {
+    const int j = j0 + l;
+    padj[l] = j >= K;
+    const int js = padj[l] ? 0 : j;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) la[i][l] = (i < K && !padj[l]) ? (R)md->log_A[i * K + js] : N::ninf();
+    em0[l].load(md->em[0][js]);
+    if (two) em1[l].load(md->em[1][js]);
+    else em1[l].fam = LOGHMM_FAM_NONE;
+  }
+  bool oob = false;
+  const double* lut = a.lut;
+  const int lut_n = a.lut_n;
+
+  int Tmax = T;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) Tmax = max(Tmax, __shfl_xor_sync(kFull, Tmax, o));
+  const int Tlast = T > 0 ? T - 1 : 0;
+
+  auto emis = [&](int l, R yv0, R yv1) -> R {
+    R lb = em0[l].eval(yv0, lut, lut_n, oob);
+    if (two) lb = N::add(lb, em1[l].eval(yv1, lut, lut_n, oob));
+    return padj[l] ? N::ninf() : lb;
+  };
+
+  // ---- forward max-plus recursion ---------------------------------------
+  R d[KL];
+#pragma unroll
+  for (int l = 0; l < KL; ++l) {
+    d[l] = N::ninf();
+    if (T > 0 && !padj[l]) d[l] = N::add((R)md->log_pi[j0 + l], emis(l, y0g[0], two ? y1g[0] : R(0)));
+  }
+  uint32_t nib = 0;  // 8 steps x (2 states x 2 bits)
+
+  auto step = [&](int t, const R (&lb)[KL]) {
+    // full score vector in natural order: lane h=0 owns 0,1; h=1 owns 2,3
+    const R o0 = __shfl_xor_sync(kFull, d[0], 1);
+    const R o1 = __shfl_xor_sync(kFull, d[1], 1);
+    R full[4];
+    full[0] = h ? o0 : d[0];
+    full[1] = h ? o1 : d[1];
+    full[2] = h ? d[0] : o0;
+    full[3] = h ? d[1] : o1;
+    const bool act = t < T;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int l = 0; l < KL; ++l) {
+      R cand[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) cand[i] = N::add(full[i], la[i][l]);
+      R best;
+      int bi;
+      ArgMax<R, 0, K>::run(cand, best, bi);
+      d[l] = act ? N::add(best, lb[l]) : d[l];
+      bits |= (uint32_t)bi << (2 * l);
+    }
+    nib |= bits << (4 * (t & 7));
+    if ((t & 7) == 7 || t == Tmax - 1) {
+      bpw[(size_t)(t >> 3) * kWarp + lane] = nib;
+      nib = 0;
+    }
+  };
+
+  constexpr int U = 8;
+  R y0a[U], y1a[U], y0b[U], y1b[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int ta = min(1 + u, Tlast), tb2 = min(1 + U + u, Tlast);
+    y0a[u] = y0g[ta];
+    y1a[u] = two ? y1g[ta] : R(0);
+    y0b[u] = y0g[tb2];
+    y1b[u] = two ? y1g[tb2] : R(0);
+  }
+  int t = 1;
+#pragma unroll 1
+  for (; t + U <= Tmax; t += U) {
+    R lbs[U][KL];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int l = 0; l < KL; ++l) lbs[u][l] = emis(l, y0a[u], y1a[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      y0a[u] = y0b[u];
+      y1a[u] = y1b[u];
+      const int tt = min(t + 2 * U + u, Tlast);
+      y0b[u] = y0g[tt];
+      y1b[u] = two ? y1g[tt] : R(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) step(t + u, lbs[u]);
+  }
+#pragma unroll 1
+  for (; t < Tmax; ++t) {
+    const int tt = min(t, Tlast);
+    R lb[KL];
+#pragma unroll
+    for (int l = 0; l < KL; ++l) lb[l] = emis(l, y0g[tt], two ? y1g[tt] : R(0));
+    step(t, lb);
+  }
+
+  // best final state (first index) and log joint
+  int best_last = 0;
+  R best_val = N::ninf();
+  {
+    const R o0 = __shfl_xor_sync(kFull, d[0], 1);
+    const R o1 = __shfl_xor_sync(kFull, d[1], 1);
+    R full[4];
+    full[0] = h ? o0 : d[0];
+    full[1] = h ? o1 : d[1];
+    full[2] = h ? d[0] : o0;
+    full[3] = h ? d[1] : o1;
+    ArgMax<R, 0, K>::run(full, best_val, best_last);
+  }
+  if (valid && h == 0) {
+    a.log_joint[b] = (double)best_val;
+    if (a.flags && oob) a.flags[2 * b + 1] |= 2;
+  }
+  __syncwarp();
+
+  // back_t[v] for sequence qq: 2 bits at (t%8)*4 + (v&1)*2 of word [t/8][2qq + (v>>1)]
+  auto tbl_of = [&](int qq, int t2) -> unsigned {
+    const uint32_t* row = bpw + (size_t)(t2 >> 3) * kWarp + 2 * qq;
+    const unsigned sh = 4u * (unsigned)(t2 & 7);
+    return ((row[0] >> sh) & 0xFu) | (((row[1] >> sh) & 0xFu) << 4);  // 2 bits per state
+  };
+
+  // optional byte table of backpointers (tests)
+  if (a.back != nullptr) {
+#pragma unroll 1
+    for (int gg = 0; gg < G; ++gg) {
+      const int64_t bb = warp_id * G + gg;
+      if (bb >= a.B) break;
+      const int Tg = __shfl_sync(kFull, T, 2 * gg);
+      const int64_t sg = __shfl_sync(kFull, start, 2 * gg);
+      for (int t2 = lane; t2 < Tg; t2 += kWarp) {
+        const unsigned tb = t2 >= 1 ? tbl_of(gg, t2) : 0u;
+#pragma unroll
+        for (int jx = 0; jx < K; ++jx) a.back[(sg + t2) * K + jx] = (uint8_t)((tb >> (2 * jx)) & 3u);
+      }
+    }
+  }
+
+  // ---- backtrace, one sequence at a time with all 32 lanes ----------------
+#pragma unroll 1
+  for (int gg = 0; gg < G; ++gg) {
+    const int64_t bb = warp_id * G + gg;
+    if (bb >= a.B) break;
+    const int Tg = __shfl_sync(kFull, T, 2 * gg);
+    const int64_t sg = __shfl_sync(kFull, start, 2 * gg);
+    const unsigned blast = (unsigned)__shfl_sync(kFull, best_last, 2 * gg);
+    if (Tg <= 0) continue;
+    const int L = (Tg + kWarp - 1) / kWarp;
+    const int t0 = lane * L;
+    const int t1 = min(t0 + L, Tg);
+    // compose the chunk map (2 bits per entry): end state -> state before t0
+    unsigned F = 0xE4u;  // identity: entries 0,1,2,3
+    {
+      const int tlo = max(t0, 1);
+      constexpr int BB = 8;
+#pragma unroll 1
+      for (int tb = t1 - 1; tb >= tlo; tb -= BB) {
+        unsigned tbs[BB];
+#pragma unroll
+        for (int u = 0; u < BB; ++u) tbs[u] = (tb - u >= tlo) ? tbl_of(gg, tb - u) : 0u;
+#pragma unroll
+        for (int u = 0; u < BB; ++u) {
+          if (tb - u < tlo) break;
+          unsigned nf = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) nf |= ((tbs[u] >> (2 * ((F >> (2 * e)) & 3u))) & 3u) << (2 * e);
+          F = nf;
+        }
+      }
+    }
+    // inclusive suffix scan of the maps: H_c = F_c o F_{c+1} o ... o F_31
+    unsigned Hm = F;
+#pragma unroll
+    for (int dd = 1; dd < kWarp; dd <<= 1) {
+      const unsigned Hn = __shfl_down_sync(kFull, Hm, dd);
+      if (lane + dd < kWarp) {
+        unsigned c = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c |= ((Hm >> (2 * ((Hn >> (2 * e)) & 3u))) & 3u) << (2 * e);
+        Hm = c;
+      }
+    }
+    unsigned Hnext = __shfl_down_sync(kFull, Hm, 1);
+    if (lane == kWarp - 1) Hnext = 0xE4u;
+    unsigned cur = (Hnext >> (2 * blast)) & 3u;
+    int64_t* out = a.path + sg;
+    const int wtop = ((L - 1) / kPathSlab) * kPathSlab;
+#pragma unroll 1
+    for (int w0 = wtop; w0 >= 0; w0 -= kPathSlab) {
+      unsigned tbs[kPathSlab];
+#pragma unroll
+      for (int u = 0; u < kPathSlab; ++u) {
+        const int tu = t0 + w0 + u;
+        tbs[u] = (tu >= 1 && tu < t1) ? tbl_of(gg, tu) : 0u;
+      }
+#pragma unroll
+      for (int u = kPathSlab - 1; u >= 0; --u) {
+        const int tu = t0 + w0 + u;
+        if (w0 + u < L && tu < t1) {
+          pstage[lane * kPathPitch + u] = (int64_t)cur;
+          if (tu >= 1) cur = (tbs[u] >> (2 * cur)) & 3u;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int rep = 0; rep < kPathSlab; ++rep) {
+        const int idx = rep * kWarp + lane;
+        const int c = idx / kPathSlab, e = idx % kPathSlab;
+        const int tt = c * L + w0 + e;
+        if (w0 + e < L && tt < Tg) out[tt] = pstage[c * kPathPitch + e];
+      }
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace lhmm

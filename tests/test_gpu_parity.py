@@ -106,7 +106,7 @@ def _near_tie_ok(lp, la, lb, t, j, ours, theirs, dtype=np.float64):
     return gap <= 64 * np.finfo(R).eps * max(1.0, abs(float(cand[theirs, j])))
 
 
-def test_viterbi_matches_reference(golden):
+def test_viterbi_matches_reference(golden, vit_algo):
     v = golden["vec"]
     for c in golden["cases"]:
         m = to_model(c["pi"], c["A"], c["emissions"])
@@ -138,8 +138,16 @@ def _random_gauss_model(rng, K):
                                    for _ in range(K)))
 
 
+@pytest.fixture(params=["auto", "klane"])
+def vit_algo(request, monkeypatch):
+    """Run a test under both Viterbi layouts (two-lane for K<=4, K-lane)."""
+    if request.param == "klane":
+        monkeypatch.setenv("LOGHMM_VIT_ALGO", "klane")
+    return request.param
+
+
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 5, 8])
-def test_fp32_viterbi_bitexact_ragged(K):
+def test_fp32_viterbi_bitexact_ragged(K, vit_algo):
     rng = np.random.default_rng(100 + K)
     m = _random_gauss_model(rng, K)
     lens = [1, 2, 31, 32, 33, 64, 100, 257, 1024, 700]
@@ -158,8 +166,8 @@ def test_fp32_viterbi_bitexact_ragged(K):
         assert lj[b] == j
 
 
-@pytest.mark.parametrize("K", [2, 4, 7])
-def test_fp64_viterbi_poisson_bitexact(K):
+@pytest.mark.parametrize("K", [2, 3, 4, 7])
+def test_fp64_viterbi_poisson_bitexact(K, vit_algo):
     rng = np.random.default_rng(7 + K)
     pi = rng.dirichlet(np.ones(K))
     A = rng.dirichlet(np.ones(K), size=K)
