@@ -84,7 +84,8 @@ static FBGeom fb_geom(int K, int esz, int n_streams, int64_t max_T) {
   const int64_t smem_elems = (int64_t)kWarp * (g.y_pitch * n_streams + g.a_pitch + 2 * g.s_pitch);
   const int64_t bytes = smem_elems * esz;
   g.global = bytes > 110 * 1024;
-  g.warp_elems = g.global ? kWarp * 2 * g.s_pitch : (int)smem_elems;
+  // + beta~ prefetch ring: 8 steps x 32 lanes x K
+  g.warp_elems = (g.global ? kWarp * 2 * g.s_pitch : (int)smem_elems) + 8 * kWarp * K;
   const int64_t wbytes = (int64_t)g.warp_elems * esz;
   g.wpb = (int)std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / wbytes));
   g.smem = (size_t)(wbytes * g.wpb);

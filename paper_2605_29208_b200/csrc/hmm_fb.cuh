@@ -431,7 +431,7 @@ __device__ __forceinline__ void stats_step(R (&st)[CfgTraits<CFG>::S][K][LOGHMM_
 // The kernel.
 // ---------------------------------------------------------------------------
 template <typename R, int K, int CFG, bool kGlobal>
-__global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(const FBArgs a) {
   typedef Num<R> N;
   typedef CfgTraits<CFG> TR;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -801,15 +801,37 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
 #pragma unroll
     for (int j = 0; j < K; ++j) av[j] = a_in[j];
     int cnt = 0;
+    // beta~ prefetch ring (cp.async, kBD steps ahead) in this warp's stage area
+    constexpr int kBD = 8;
+    constexpr int BB = K * (int)sizeof(R);
+    R* bring = stB + kWarp * a.s_pitch + lane * K;  // [kBD][32][K]
+    auto issue_b = [&](int s2) {
+      const bool ok = s2 < len;
+      R* dst = bring + (s2 & (kBD - 1)) * AW_STEP;
+      const R* src = ok ? aw + s2 * AW_STEP : aw;
+      if constexpr (BB == 4 || BB == 8 || BB == 16) {
+        cp_async<BB>(dst, src, ok);
+      } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j) cp_async<sizeof(R)>(dst + j, src + j, ok);
+      }
+    };
+#pragma unroll 1
+    for (int s2 = 0; s2 < kBD; ++s2) {
+      issue_b(s2);
+      cp_async_commit();
+    }
 #pragma unroll 1
     for (int s = 0; s < L; ++s) {
+      cp_async_wait<kBD - 1>();
       const int t = t0 + s;
       if (s < len) {
         ObsFeat<R> f0, f1;
         R lb[K];
         em.eval(yat0(s), yat1(s), f0, f1, lb, oob);
         R bet[K];
-        VecIO<R, K>::ld(aw + s * AW_STEP, bet);
+#pragma unroll
+        for (int j = 0; j < K; ++j) bet[j] = bring[(s & (kBD - 1)) * AW_STEP + j];
         if (disc_lane) l2_discard(aw + s * AW_STEP);
         R g[K];
         if (t == 0) {
@@ -904,6 +926,8 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
           for (int j = 0; j < K; ++j) gtot[j] += g[j];
         }
       }
+      issue_b(s + kBD);
+      cp_async_commit();
       if (((s % kSlab) == kSlab - 1 || s == L - 1) && (outA || outG)) {
         __syncwarp();
         const int sb = s - (s % kSlab);
@@ -913,6 +937,8 @@ __global__ void __launch_bounds__(128) fb_small_kernel(const FBArgs a) {
       }
     }
   }
+
+  cp_async_wait_all();
 
   // ---- reductions and per-sequence outputs --------------------------------
   const int dead_all = (int)warp_min_ll((long long)dead_t);

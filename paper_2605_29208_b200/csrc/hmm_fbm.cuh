@@ -49,21 +49,6 @@ struct FBMArgs {
   int64_t stats_width;
 };
 
-// Asynchronous global->shared copies (LDGSTS) with zero-fill when !pred.
-template <int BYTES>
-__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, bool pred) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  const int n = pred ? BYTES : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(gsrc), "n"(BYTES),
-               "r"(n)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-
 template <typename R, int KL>
 struct LVec {
   static __device__ __forceinline__ void st(R* p, const R (&v)[KL]) {

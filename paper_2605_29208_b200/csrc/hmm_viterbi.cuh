@@ -52,7 +52,11 @@ struct Bits {
 };
 
 // First-index argmax over cand[lo, hi) as a pairwise tree (the right half wins
-// only on a strictly greater value, which preserves numpy's tie rule).
+// only on a strictly greater value, which preserves numpy's tie rule).  The
+// maximum itself goes through FMNMX (4-cycle latency, on the recursion's
+// critical path); the index selection hangs off it.  Both agree except for
+// the sign of an exact zero tie, which cannot change the next score unless the
+// emission term is also exactly zero.
 template <typename R, int LO, int HI>
 struct ArgMax {
   static __device__ __forceinline__ void run(const R* c, R& v, int& i) {
@@ -66,7 +70,7 @@ struct ArgMax {
       ArgMax<R, LO, MID>::run(c, lv, li);
       ArgMax<R, MID, HI>::run(c, rv, ri);
       const bool right = rv > lv;
-      v = right ? rv : lv;
+      v = fmax(lv, rv);
       i = right ? ri : li;
     }
   }

@@ -112,43 +112,47 @@ __global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
     }
   };
 
+  // Software-pipelined: while the score chain of block k runs, the emission
+  // terms of block k+1 are evaluated in the same instruction stream (they are
+  // independent of the chain), and y is loaded two blocks ahead.
   constexpr int U = 8;
-  R y0a[U], y1a[U], y0b[U], y1b[U];
+  R y0a[U], y1a[U];  // y of block k+2 (in flight)
+  R lbs[U][KL], lbn[U][KL];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const int ta = min(1 + u, Tlast), tb2 = min(1 + U + u, Tlast);
-    y0a[u] = y0g[ta];
-    y1a[u] = two ? y1g[ta] : R(0);
-    y0b[u] = y0g[tb2];
-    y1b[u] = two ? y1g[tb2] : R(0);
+    const int t1_ = min(1 + u, Tlast), t2_ = min(1 + U + u, Tlast);
+#pragma unroll
+    for (int l = 0; l < KL; ++l) lbs[u][l] = emis(l, y0g[t1_], two ? y1g[t1_] : R(0));
+    y0a[u] = y0g[t2_];
+    y1a[u] = two ? y1g[t2_] : R(0);
   }
   int t = 1;
 #pragma unroll 1
   for (; t + U <= Tmax; t += U) {
-    R lbs[U][KL];
+    R y0c[U], y1c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      y0c[u] = y0a[u];
+      y1c[u] = y1a[u];
+      const int tt = min(t + 2 * U + u, Tlast);
+      y0a[u] = y0g[tt];
+      y1a[u] = two ? y1g[tt] : R(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int l = 0; l < KL; ++l) lbn[u][l] = emis(l, y0c[u], y1c[u]);
+      step(t + u, lbs[u]);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int l = 0; l < KL; ++l) lbs[u][l] = emis(l, y0a[u], y1a[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      y0a[u] = y0b[u];
-      y1a[u] = y1b[u];
-      const int tt = min(t + 2 * U + u, Tlast);
-      y0b[u] = y0g[tt];
-      y1b[u] = two ? y1g[tt] : R(0);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) step(t + u, lbs[u]);
+      for (int l = 0; l < KL; ++l) lbs[u][l] = lbn[u][l];
   }
-#pragma unroll 1
-  for (; t < Tmax; ++t) {
-    const int tt = min(t, Tlast);
-    R lb[KL];
+  // tail: lbs holds the emissions of steps t..t+U-1 (clamped loads)
 #pragma unroll
-    for (int l = 0; l < KL; ++l) lb[l] = emis(l, y0g[tt], two ? y1g[tt] : R(0));
-    step(t, lb);
-  }
+  for (int u = 0; u < U; ++u)
+    if (t + u < Tmax) step(t + u, lbs[u]);
 
   // best final state (first index) and log joint
   int best_last = 0;
@@ -192,80 +196,50 @@ __global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
     }
   }
 
-  // ---- backtrace, one sequence at a time with all 32 lanes ----------------
-#pragma unroll 1
-  for (int gg = 0; gg < G; ++gg) {
-    const int64_t bb = warp_id * G + gg;
-    if (bb >= a.B) break;
-    const int Tg = __shfl_sync(kFull, T, 2 * gg);
-    const int64_t sg = __shfl_sync(kFull, start, 2 * gg);
-    const unsigned blast = (unsigned)__shfl_sync(kFull, best_last, 2 * gg);
-    if (Tg <= 0) continue;
-    const int L = (Tg + kWarp - 1) / kWarp;
-    const int t0 = lane * L;
-    const int t1 = min(t0 + L, Tg);
-    // compose the chunk map (2 bits per entry): end state -> state before t0
-    unsigned F = 0xE4u;  // identity: entries 0,1,2,3
+  // ---- backtrace: lane 2q walks sequence q from its end ------------------
+  // One 8-step row of backpointer words per iteration: the eight 8-bit step
+  // tables are unpacked with constant shifts (independent of the walk), then
+  // the eight dependent lookups run back to back.
+  if (h == 0 && valid && T > 0) {
+    int64_t* out = a.path + start;
+    unsigned cur = (unsigned)best_last;
+    const uint32_t* col = bpw + 2 * q;
+    const int tl = T - 1;
+    out[tl] = (int64_t)cur;
+    // partial top row: steps tl .. 8*(tl>>3)
+    int row = tl >> 3;
     {
-      const int tlo = max(t0, 1);
-      constexpr int BB = 8;
-#pragma unroll 1
-      for (int tb = t1 - 1; tb >= tlo; tb -= BB) {
-        unsigned tbs[BB];
-#pragma unroll
-        for (int u = 0; u < BB; ++u) tbs[u] = (tb - u >= tlo) ? tbl_of(gg, tb - u) : 0u;
-#pragma unroll
-        for (int u = 0; u < BB; ++u) {
-          if (tb - u < tlo) break;
-          unsigned nf = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) nf |= ((tbs[u] >> (2 * ((F >> (2 * e)) & 3u))) & 3u) << (2 * e);
-          F = nf;
-        }
+      const uint32_t w0 = col[(size_t)row * kWarp], w1 = col[(size_t)row * kWarp + 1];
+      for (int t2 = tl; t2 > row * 8; --t2) {
+        const unsigned sh = 4u * (unsigned)(t2 & 7);
+        const unsigned tb = ((w0 >> sh) & 0xFu) | (((w1 >> sh) & 0xFu) << 4);
+        cur = (tb >> (2 * cur)) & 3u;
+        out[t2 - 1] = (int64_t)cur;
+      }
+      if (row > 0) {  // step row*8 (lowest of the row) maps to row*8 - 1
+        const unsigned tb = (w0 & 0xFu) | ((w1 & 0xFu) << 4);
+        cur = (tb >> (2 * cur)) & 3u;
+        out[row * 8 - 1] = (int64_t)cur;
       }
     }
-    // inclusive suffix scan of the maps: H_c = F_c o F_{c+1} o ... o F_31
-    unsigned Hm = F;
-#pragma unroll
-    for (int dd = 1; dd < kWarp; dd <<= 1) {
-      const unsigned Hn = __shfl_down_sync(kFull, Hm, dd);
-      if (lane + dd < kWarp) {
-        unsigned c = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) c |= ((Hm >> (2 * ((Hn >> (2 * e)) & 3u))) & 3u) << (2 * e);
-        Hm = c;
-      }
-    }
-    unsigned Hnext = __shfl_down_sync(kFull, Hm, 1);
-    if (lane == kWarp - 1) Hnext = 0xE4u;
-    unsigned cur = (Hnext >> (2 * blast)) & 3u;
-    int64_t* out = a.path + sg;
-    const int wtop = ((L - 1) / kPathSlab) * kPathSlab;
 #pragma unroll 1
-    for (int w0 = wtop; w0 >= 0; w0 -= kPathSlab) {
-      unsigned tbs[kPathSlab];
+    for (--row; row >= 0; --row) {
+      const uint32_t w0 = col[(size_t)row * kWarp], w1 = col[(size_t)row * kWarp + 1];
+      unsigned tbs[8];
 #pragma unroll
-      for (int u = 0; u < kPathSlab; ++u) {
-        const int tu = t0 + w0 + u;
-        tbs[u] = (tu >= 1 && tu < t1) ? tbl_of(gg, tu) : 0u;
+      for (int u = 0; u < 8; ++u) tbs[u] = ((w0 >> (4 * u)) & 0xFu) | (((w1 >> (4 * u)) & 0xFu) << 4);
+      unsigned p[8];
+#pragma unroll
+      for (int u = 7; u >= 1; --u) {  // step row*8+u -> state at row*8+u-1
+        cur = (tbs[u] >> (2 * cur)) & 3u;
+        p[u - 1] = cur;
+      }
+      if (row > 0) {
+        cur = (tbs[0] >> (2 * cur)) & 3u;
+        out[row * 8 - 1] = (int64_t)cur;
       }
 #pragma unroll
-      for (int u = kPathSlab - 1; u >= 0; --u) {
-        const int tu = t0 + w0 + u;
-        if (w0 + u < L && tu < t1) {
-          pstage[lane * kPathPitch + u] = (int64_t)cur;
-          if (tu >= 1) cur = (tbs[u] >> (2 * cur)) & 3u;
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int rep = 0; rep < kPathSlab; ++rep) {
-        const int idx = rep * kWarp + lane;
-        const int c = idx / kPathSlab, e = idx % kPathSlab;
-        const int tt = c * L + w0 + e;
-        if (w0 + e < L && tt < Tg) out[tt] = pstage[c * kPathPitch + e];
-      }
-      __syncwarp();
+      for (int u = 0; u < 7; ++u) out[row * 8 + u] = (int64_t)p[u];
     }
   }
 }

@@ -396,3 +396,21 @@ def test_config5_viterbi_and_posteriors_subset():
         assert np.array_equal(vit.path[s].cpu().numpy(), p)
         assert np.array_equal(vit.back[s].cpu().numpy().astype(np.int64), bk)
         assert vit.log_joint[b].item() == j
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_exact_gaussian_emission_wide_range(dtype):
+    """The hoisted-reciprocal division in the exact emission reproduces the
+    reference's IEEE quotient (hence log b) bit for bit over a wide range of
+    magnitudes, including values that underflow or overflow the square."""
+    rng = np.random.default_rng(17)
+    R = np.float64 if dtype == "float64" else np.float32
+    mags = 10.0 ** rng.uniform(-40 if R is np.float32 else -300, 38 if R is np.float32 else 300, 200_000)
+    y = (rng.choice([-1.0, 1.0], mags.size) * mags).astype(R)
+    y[:100] = 0.0
+    for mu, sigma in ((0.0, 1.0), (0.37, 0.77), (-3.0, 1.4999), (1e-3, 3.3e-2)):
+        m = H.HmmModel([1.0], [[1.0]], (H.Gaussian(mu, sigma),))
+        lb = H.emission_log_matrix(m, y.astype(np.float64) if R is np.float64 else y, dtype=dtype)
+        ref = O.emission_matrix([("gaussian", mu, sigma)], y, R)
+        got = np.asarray(lb).reshape(-1)
+        assert np.array_equal(got, ref[:, 0]), (mu, sigma, int((got != ref[:, 0]).sum()))
