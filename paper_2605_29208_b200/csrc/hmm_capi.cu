@@ -100,15 +100,18 @@ struct VitGeom {
   size_t smem;
 };
 
-static VitGeom vit_geom(int K, int64_t max_T) {
+// esz: element size of the observations; ns: observation streams staged by
+// the kernel instantiation (2 for the two-stream configurations).
+static VitGeom vit_geom(int K, int64_t max_T, int esz = 8, int ns = 2) {
   VitGeom g{};
-  const int NP = K <= 1 ? 0 : K <= 2 ? 1 : K <= 4 ? 2 : 3;
-  g.plane_words = ((max_T + 31) / 32) * 32 * std::max(NP, 1);
-  const int64_t stage_words = 2 * kWarp * kPathPitch;
-  g.global = g.plane_words > 12 * 1024;  // > 48 KB of planes per warp
+  // steps are processed in whole 32-step chunks: room for 32 * ceil(T/32) + 1
+  // steps (plus one step of slack for the table reads), kStepWords words each
+  g.plane_words = ((max_T + 31) / 32 + 2) * 32 * kStepWords;
+  const int64_t stage_words = vit_stage_words(K, esz, ns);
+  g.global = g.plane_words > 12 * 1024;  // > 48 KB of step tables per warp
   g.warp_words = (int)(stage_words + (g.global ? 0 : g.plane_words));
   g.warp_words = (g.warp_words + 3) & ~3;
-  g.wpb = 4;
+  g.wpb = (int)std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / ((int64_t)g.warp_words * 4)));
   g.smem = (size_t)g.warp_words * 4 * g.wpb;
   return g;
 }
@@ -128,12 +131,14 @@ static cudaError_t dispatch_fb_small(int K, const FBArgs& a, int cfg, bool gl, d
   }
 }
 
-// Two-lane Viterbi (K in [2,4]) geometry: nibble backpointer words in smem.
+// Two-lane Viterbi (K in [2,4], LOGHMM_VIT_ALGO=pair) geometry: nibble
+// backpointer words in smem.  Kept as an alternative decomposition; the K-lane
+// kernel is faster on B200 (twice the warps, shorter per-step issue).
 static bool vit2_ok(int K, int64_t max_T, int* wpb, size_t* smem, int* warp_words) {
   if (K < 2 || K > 4) return false;
   const char* env = getenv("LOGHMM_VIT_ALGO");
-  if (env && strcmp(env, "klane") == 0) return false;
-  const int64_t words = 2 * kWarp * kPathPitch + ((max_T + 7) / 8) * kWarp;
+  if (!env || strcmp(env, "pair") != 0) return false;  // K-lane kernel is the default
+  const int64_t words = kVit2StageWords + ((max_T + 7) / 8) * kWarp;
   const int64_t bytes = ((words + 3) & ~3LL) * 4;
   if (bytes > 100 * 1024) return false;
   *warp_words = (int)((words + 3) & ~3LL);
@@ -383,15 +388,16 @@ int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm
     e = dtype == LOGHMM_F64 ? dispatch_vit2<double>(K, a, cfg, grid, block, v2_smem, st)
                             : dispatch_vit2<float>(K, a, cfg, grid, block, v2_smem, st);
   } else if (K <= 8) {
-    VitGeom g = vit_geom(K, max_T);
+    int fams = 0;
+    const int cfg = cfg_of(h_desc, &fams);
+    const int ns = (cfg == kCfgGammaVM || cfg == kCfgMixed) ? 2 : 1;
+    VitGeom g = vit_geom(K, max_T, dtype == LOGHMM_F64 ? 8 : 4, ns);
     a.planes_ws = (uint32_t*)workspace;
     a.plane_words = g.plane_words;
     a.warp_smem_words = g.warp_words;
     const int64_t G = kWarp / K;
     const int64_t warps = (B + G - 1) / G;
     dim3 grid((unsigned)((warps + g.wpb - 1) / g.wpb)), block(32 * g.wpb);
-    int fams = 0;
-    const int cfg = cfg_of(h_desc, &fams);
     e = dtype == LOGHMM_F64 ? dispatch_vit_small<double>(K, a, cfg, g.global, grid, block, g.smem, st)
                             : dispatch_vit_small<float>(K, a, cfg, g.global, grid, block, g.smem, st);
   } else {

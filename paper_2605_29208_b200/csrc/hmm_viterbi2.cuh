@@ -13,6 +13,10 @@
 
 namespace lhmm {
 
+// shared words per warp ahead of the backpointer words: [16][33] int64 path
+// staging, then the {T, start} table of the 16 sequences
+constexpr int kVit2StageWords = 2 * 16 * kStagePitch + 16 * 3 + 4;
+
 template <typename R, int K, int CFG>
 __global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
   static_assert(K >= 2 && K <= 4, "two-lane Viterbi covers 2 <= K <= 4");
@@ -32,8 +36,8 @@ __global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
   if (warp_id * G >= a.B) return;
 
   uint32_t* wsm = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wib * a.warp_smem_words;
-  int64_t* pstage = reinterpret_cast<int64_t*>(wsm);  // kWarp * kPathPitch int64
-  uint32_t* bpw = kWarp * kPathPitch * 2 + wsm;         // [ceil(Tmax/8)][32] nibble words
+  int64_t* pstage = reinterpret_cast<int64_t*>(wsm);  // path staging + sequence table
+  uint32_t* bpw = kVit2StageWords + wsm;                // [ceil(Tmax/8)][32] nibble words
 
   const loghmm_model_t* __restrict__ md = a.model;
   const int64_t start = valid ? a.offsets[b] : 0;
@@ -197,50 +201,53 @@ __global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
   }
 
   // ---- backtrace: lane 2q walks sequence q from its end ------------------
-  // One 8-step row of backpointer words per iteration: the eight 8-bit step
-  // tables are unpacked with constant shifts (independent of the walk), then
-  // the eight dependent lookups run back to back.
-  if (h == 0 && valid && T > 0) {
-    int64_t* out = a.path + start;
-    unsigned cur = (unsigned)best_last;
-    const uint32_t* col = bpw + 2 * q;
-    const int tl = T - 1;
-    out[tl] = (int64_t)cur;
-    // partial top row: steps tl .. 8*(tl>>3)
-    int row = tl >> 3;
-    {
-      const uint32_t w0 = col[(size_t)row * kWarp], w1 = col[(size_t)row * kWarp + 1];
-      for (int t2 = tl; t2 > row * 8; --t2) {
-        const unsigned sh = 4u * (unsigned)(t2 & 7);
-        const unsigned tb = ((w0 >> sh) & 0xFu) | (((w1 >> sh) & 0xFu) << 4);
-        cur = (tb >> (2 * cur)) & 3u;
-        out[t2 - 1] = (int64_t)cur;
-      }
-      if (row > 0) {  // step row*8 (lowest of the row) maps to row*8 - 1
-        const unsigned tb = (w0 & 0xFu) | ((w1 & 0xFu) << 4);
-        cur = (tb >> (2 * cur)) & 3u;
-        out[row * 8 - 1] = (int64_t)cur;
-      }
-    }
+  // Warp-uniform windows of 32 steps (four 8-step rows of backpointer words)
+  // from the top: per row the eight 8-bit step tables are unpacked with
+  // constant shifts (independent of the walk), the dependent lookups run back
+  // to back, and the states are staged in shared memory [q][32]; each window
+  // is then written with one coalesced 256-byte store per sequence.
+  int64_t* stage = pstage;                                            // [G][kStagePitch]
+  int2* seqtab = reinterpret_cast<int2*>(pstage + G * kStagePitch);  // [G] {T, start lo}
+  int* seqhi = reinterpret_cast<int*>(seqtab + G);                   // [G] start hi
+  if (h == 0) {
+    seqtab[q] = make_int2(valid ? T : 0, (int)(uint32_t)start);
+    seqhi[q] = (int)(start >> 32);
+  }
+  __syncwarp();
+  unsigned cur = (unsigned)best_last;
+  const bool walker = h == 0 && valid;
+  const uint32_t* col = bpw + 2 * q;
+  const int wtop = Tmax > 0 ? (Tmax - 1) >> 5 : -1;
 #pragma unroll 1
-    for (--row; row >= 0; --row) {
-      const uint32_t w0 = col[(size_t)row * kWarp], w1 = col[(size_t)row * kWarp + 1];
-      unsigned tbs[8];
+  for (int w = wtop; w >= 0; --w) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) tbs[u] = ((w0 >> (4 * u)) & 0xFu) | (((w1 >> (4 * u)) & 0xFu) << 4);
-      unsigned p[8];
+    for (int r = 3; r >= 0; --r) {
+      const int row = 4 * w + r;
+      if (walker && row * 8 < T) {
+        const uint32_t w0 = col[(size_t)row * kWarp], w1 = col[(size_t)row * kWarp + 1];
+        unsigned tbs[8];
 #pragma unroll
-      for (int u = 7; u >= 1; --u) {  // step row*8+u -> state at row*8+u-1
-        cur = (tbs[u] >> (2 * cur)) & 3u;
-        p[u - 1] = cur;
+        for (int u = 0; u < 8; ++u) tbs[u] = ((w0 >> (4 * u)) & 0xFu) | (((w1 >> (4 * u)) & 0xFu) << 4);
+#pragma unroll
+        for (int u = 7; u >= 0; --u) {
+          if (row * 8 + u < T) {  // step row*8+u holds cur; its table gives step -1
+            stage[q * kStagePitch + r * 8 + u] = (int64_t)cur;
+            cur = (tbs[u] >> (2 * cur)) & 3u;
+          }
+        }
       }
-      if (row > 0) {
-        cur = (tbs[0] >> (2 * cur)) & 3u;
-        out[row * 8 - 1] = (int64_t)cur;
-      }
-#pragma unroll
-      for (int u = 0; u < 7; ++u) out[row * 8 + u] = (int64_t)p[u];
     }
+    __syncwarp();
+#pragma unroll 4
+    for (int qq = 0; qq < G; ++qq) {
+      const int2 e = seqtab[qq];
+      const int tt = w * 32 + lane;
+      if (tt < e.x) {
+        const int64_t st = ((int64_t)seqhi[qq] << 32) | (uint32_t)e.y;
+        a.path[st + tt] = stage[qq * kStagePitch + lane];
+      }
+    }
+    __syncwarp();
   }
 }
 

@@ -138,11 +138,11 @@ def _random_gauss_model(rng, K):
                                    for _ in range(K)))
 
 
-@pytest.fixture(params=["auto", "klane"])
+@pytest.fixture(params=["auto", "pair"])
 def vit_algo(request, monkeypatch):
     """Run a test under both Viterbi layouts (two-lane for K<=4, K-lane)."""
-    if request.param == "klane":
-        monkeypatch.setenv("LOGHMM_VIT_ALGO", "klane")
+    if request.param == "pair":
+        monkeypatch.setenv("LOGHMM_VIT_ALGO", "pair")
     return request.param
 
 
