@@ -193,6 +193,20 @@ int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64
                      double var_ratio, loghmm_model_t* model_out, int32_t* status,
                      double* guard_state, void* stream);
 
+/* Fused single-rank reduction + M-step: the fixed-order block reduction of
+ * partials[B, width] / ll[B] into totals[width + 1] followed, in the same
+ * launch, by the M-step of loghmm_mstep (model_in == NULL: reduction only).
+ * Replaces the loghmm_reduce_stats -> loghmm_mstep pair when no cross-rank
+ * all-reduce sits between them.  The workspace (loghmm_reduce_workspace_bytes)
+ * must be zero-filled before its first use; the kernel leaves it reusable. */
+size_t loghmm_reduce_workspace_bytes(int64_t B, int64_t width);
+int32_t loghmm_reduce_mstep(const double* partials, const double* ll, int64_t B, int64_t width,
+                            double* totals, const loghmm_model_t* model_in, int64_t n_sequences,
+                            double collapse_epsilon, double nu_ceiling, double nu_tol,
+                            int32_t max_newton, double var_ratio, loghmm_model_t* model_out,
+                            int32_t* status, double* guard_state, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
 /* Exact second pass for the variance-type statistics (distributions.py:616-620
  * two-pass variance, :1051 ECME scale).  The E-step accumulates sums shifted
  * about the current parameters; when the M-step finds the new mean moved by
@@ -200,7 +214,9 @@ int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64
  * one-pass difference would lose precision) it flags the state and this call
  * recomputes sum_w (y - mean)^2 from y and gamma and finishes the fit.  Cheap
  * no-op when nothing is flagged.  Call after loghmm_mstep, before
- * loghmm_student_guard. */
+ * loghmm_student_guard.  One launch: the last block to finish reduces the
+ * block partials and finishes the flagged states; the workspace
+ * (loghmm_guard_workspace_bytes) must be zero-filled before its first use. */
 int32_t loghmm_variance_pass(int32_t dtype, loghmm_model_t* model_out, const void* y,
                              const void* gamma, int64_t N, int32_t K, int32_t stream_index,
                              const double* guard_state, int32_t* status, void* workspace,

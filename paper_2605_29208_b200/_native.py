@@ -93,6 +93,9 @@ _SIGNATURES = {
     ),
     "loghmm_reduce_stats": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "loghmm_mstep": (_i32, [_vp, _vp, _i64, _f64, _f64, _f64, _i32, _f64, _vp, _vp, _vp, _vp]),
+    "loghmm_reduce_workspace_bytes": (_sz, [_i64, _i64]),
+    "loghmm_reduce_mstep": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _f64, _f64, _f64, _i32,
+                                   _f64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "loghmm_variance_pass": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
     "loghmm_guard_workspace_bytes": (_sz, [_i32, _i64]),
     "loghmm_student_guard": (

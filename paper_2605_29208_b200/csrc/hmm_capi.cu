@@ -424,16 +424,57 @@ int32_t loghmm_reduce_stats(const double* partials, const double* ll, int64_t B,
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 
+// per-block partial sums of the guard / variance passes; the pass counter
+// (zero-initialised workspace, reset by the last block) follows them
+static inline size_t kGuardPartBytes(int K) {
+  return (size_t)148 * 4 * K * LOGHMM_GUARD_CANDIDATES * sizeof(double);
+}
+
 int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64_t n_sequences,
                      double collapse_epsilon, double nu_ceiling, double nu_tol, int32_t max_newton,
                      double var_ratio, loghmm_model_t* model_out, int32_t* status,
                      double* guard_state, void* stream) {
   if (!model_in || !totals || !model_out || !status || !guard_state || n_sequences < 1)
     return LOGHMM_EINVAL;
-  mstep_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(model_in, totals, n_sequences,
-                                                    collapse_epsilon, nu_ceiling, nu_tol,
-                                                    max_newton, model_out, status, guard_state,
-                                                    var_ratio);
+  // the widest statistics vector (K = LOGHMM_MAX_STATES) fits the default
+  // 48 KB dynamic shared-memory window
+  const int64_t wmax = (int64_t)loghmm_stats_width(LOGHMM_MAX_STATES, 2) + 1;
+  mstep_kernel<<<1, 256, (size_t)wmax * sizeof(double), (cudaStream_t)stream>>>(
+      model_in, totals, wmax, n_sequences, collapse_epsilon, nu_ceiling, nu_tol, max_newton,
+      model_out, status, guard_state, var_ratio);
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+static constexpr int kReduceBlocks = 128;
+
+size_t loghmm_reduce_workspace_bytes(int64_t B, int64_t width) {
+  (void)B;
+  return align256((size_t)kReduceBlocks * (size_t)(width + 1) * sizeof(double)) + 256;
+}
+
+int32_t loghmm_reduce_mstep(const double* partials, const double* ll, int64_t B, int64_t width,
+                            double* totals, const loghmm_model_t* model_in, int64_t n_sequences,
+                            double collapse_epsilon, double nu_ceiling, double nu_tol,
+                            int32_t max_newton, double var_ratio, loghmm_model_t* model_out,
+                            int32_t* status, double* guard_state, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  if (!partials || !ll || !totals || B < 1 || width < 0) return LOGHMM_EINVAL;
+  const bool do_mstep = model_in != nullptr;
+  if (do_mstep && (!model_out || !status || !guard_state || n_sequences < 1)) return LOGHMM_EINVAL;
+  if (!workspace || workspace_bytes < loghmm_reduce_workspace_bytes(B, width))
+    return LOGHMM_EWORKSPACE;
+  double* part = (double*)workspace;
+  unsigned* counter =
+      (unsigned*)((char*)workspace + align256((size_t)kReduceBlocks * (size_t)(width + 1) * 8));
+  const size_t smem = (size_t)(width + 1) * sizeof(double);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(reduce_mstep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
+    return LOGHMM_ELAUNCH;
+  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(kReduceBlocks, B));
+  reduce_mstep_kernel<<<nb, 256, smem, (cudaStream_t)stream>>>(
+      partials, ll, B, width, part, counter, totals, model_in, n_sequences, collapse_epsilon,
+      nu_ceiling, nu_tol, max_newton, model_out, status, guard_state, var_ratio, do_mstep ? 1 : 0);
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 
@@ -444,24 +485,23 @@ int32_t loghmm_variance_pass(int32_t dtype, loghmm_model_t* model_out, const voi
   if (!model_out || !y || !gamma || !guard_state || !status || K < 1) return LOGHMM_EINVAL;
   if (workspace_bytes < loghmm_guard_workspace_bytes(K, N)) return LOGHMM_EWORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  const int nblocks = 148 * 4;
+  const int nblocks = 148 * 2;
   double* part = (double*)workspace;
+  unsigned* counter = (unsigned*)((char*)workspace + kGuardPartBytes(K));
   if (dtype == LOGHMM_F64)
     variance_pass_kernel<double><<<nblocks, 256, 0, st>>>((const double*)y, (const double*)gamma, N,
                                                           K, stream_index, model_out, guard_state,
-                                                          part);
+                                                          part, counter, status);
   else
     variance_pass_kernel<float><<<nblocks, 256, 0, st>>>((const float*)y, (const float*)gamma, N, K,
                                                          stream_index, model_out, guard_state,
-                                                         part);
-  variance_finish_kernel<<<1, 64, 0, st>>>(model_out, K, stream_index, guard_state, part, nblocks,
-                                           status);
+                                                         part, counter, status);
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 
 size_t loghmm_guard_workspace_bytes(int32_t K, int64_t N) {
   (void)N;
-  return align256((size_t)148 * 4 * K * LOGHMM_GUARD_CANDIDATES * sizeof(double) + 16);
+  return align256(kGuardPartBytes(K) + 16);
 }
 
 int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const void* y0,

@@ -2,13 +2,31 @@
 // (dtype, K) in inst_*.cu so the heavy kernel bodies compile in parallel.
 #pragma once
 
+// Translation units that instantiate one kernel family define LHMM_ONLY_FB,
+// LHMM_ONLY_VIT or LHMM_ONLY_FBM first, so they depend on (and parse) only
+// that family's header; hmm_capi.cu sees every declaration.
+#if defined(LHMM_ONLY_FB)
+#include "hmm_fb.cuh"
+#define LHMM_HAS_FB 1
+#elif defined(LHMM_ONLY_VIT)
+#include "hmm_viterbi2.cuh"
+#define LHMM_HAS_VIT 1
+#elif defined(LHMM_ONLY_FBM)
+#include "hmm_fbm.cuh"
+#define LHMM_HAS_FBM 1
+#else
 #include "hmm_fb.cuh"
 #include "hmm_fbm.cuh"
 #include "hmm_viterbi.cuh"
 #include "hmm_viterbi2.cuh"
+#define LHMM_HAS_FB 1
+#define LHMM_HAS_VIT 1
+#define LHMM_HAS_FBM 1
+#endif
 
 namespace lhmm {
 
+#if defined(LHMM_HAS_FB)
 template <typename R, int K, int CFG, bool G>
 static cudaError_t launch_fb_one(const FBArgs& a, dim3 grid, dim3 block, size_t smem,
                                  cudaStream_t st) {
@@ -39,7 +57,9 @@ cudaError_t launch_fb_small(const FBArgs& a, int cfg, bool global, dim3 grid, di
   return global ? launch_fb_cfg<R, K, true>(a, cfg, grid, block, smem, st)
                 : launch_fb_cfg<R, K, false>(a, cfg, grid, block, smem, st);
 }
+#endif  // LHMM_HAS_FB
 
+#if defined(LHMM_HAS_VIT)
 template <typename R, int K, int CFG, bool G>
 static cudaError_t launch_vit_one(const VitArgs& a, dim3 grid, dim3 block, size_t smem,
                                   cudaStream_t st) {
@@ -98,7 +118,9 @@ cudaError_t launch_vit2(const VitArgs& a, int cfg, dim3 grid, dim3 block, size_t
     default: return launch_vit2_one<R, K, kCfgMixed>(a, grid, block, smem, st);
   }
 }
+#endif  // LHMM_HAS_VIT
 
+#if defined(LHMM_HAS_FBM)
 template <typename R, int K, int CFG>
 static cudaError_t launch_fbm_one(const FBMArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   auto fn = fb_mitm_kernel<R, K, CFG>;
@@ -123,6 +145,7 @@ cudaError_t launch_fb_mitm(const FBMArgs& a, int cfg, dim3 grid, size_t smem, cu
 
 template <typename R, int K>
 size_t fb_mitm_smem() { return MISmem<R, K>::bytes(); }
+#endif  // LHMM_HAS_FBM
 
 #define LHMM_INST_FB(R, K)                                                                   \
   template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \

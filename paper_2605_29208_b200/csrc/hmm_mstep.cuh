@@ -198,14 +198,13 @@ __global__ void __launch_bounds__(256) reduce_stats_kernel(const double* __restr
 //  [13]    n (total weight),  [14] sum w log y (gamma),  [15] old shape (gamma)
 constexpr int kGuardStride = 16;
 
-__global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const double* __restrict__ tot,
-                             int64_t nseq, double eps, double nu_ceiling, double nu_tol,
-                             int max_newton, loghmm_model_t* __restrict__ mout,
-                             int32_t* __restrict__ status, double* __restrict__ guard,
-                             double var_ratio) {
+__device__ void mstep_body(const loghmm_model_t* __restrict__ min_, const double* __restrict__ tot,
+                           int64_t nseq, double eps, double nu_ceiling, double nu_tol,
+                           int max_newton, loghmm_model_t* __restrict__ mout,
+                           int32_t* __restrict__ status, double* __restrict__ guard,
+                           double var_ratio, int tid, int nthreads) {
   const int K = min_->K;
   const int S = min_->n_streams;
-  const int tid = threadIdx.x;
   const int width_xi = K * K;
   const double* xi = tot;
   const double* gt = tot + width_xi;
@@ -217,20 +216,16 @@ __global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const doub
   }
   // ---- transitions and initial distribution (training.py:105-127) ----
   if (tid < K) {
+    // row i: A[i, :] = xi[i, :] / gt[i], renormalised (no read-back of mout)
     const int i = tid;
-    double row[LOGHMM_MAX_STATES];
-    for (int j = 0; j < K; ++j) mout->A[i * K + j] = min_->A[i * K + j];
-    if (gt[i] >= eps) {
-      double total = 0.0;
-      for (int j = 0; j < K; ++j) {
-        row[j] = xi[i * K + j] / gt[i];
-        total += row[j];
-      }
-      if (total > 0.0)
-        for (int j = 0; j < K; ++j) mout->A[i * K + j] = row[j] / total;
-    }
+    const double g = gt[i];
+    double total = 0.0;
+    if (g >= eps)
+      for (int j = 0; j < K; ++j) total += xi[i * K + j] / g;
+    const bool upd = g >= eps && total > 0.0;
     for (int j = 0; j < K; ++j) {
-      const double v = mout->A[i * K + j];
+      const double v = upd ? (xi[i * K + j] / g) / total : min_->A[i * K + j];
+      mout->A[i * K + j] = v;
       mout->log_A[i * K + j] = v > 0.0 ? log(v) : -CUDART_INF;
     }
   }
@@ -244,7 +239,7 @@ __global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const doub
     }
   }
   // ---- emissions (training.py:130-148 -> distributions.py:1094 refit) ----
-  for (int idx = tid; idx < S * K; idx += blockDim.x) {
+  for (int idx = tid; idx < S * K; idx += nthreads) {
     const int s = idx / K, j = idx % K;
     loghmm_emission_t e = min_->em[s][j];
     const double* q = em + (size_t)(s * K + j) * LOGHMM_NSLOT;
@@ -430,6 +425,71 @@ __global__ void mstep_kernel(const loghmm_model_t* __restrict__ min_, const doub
   }
 }
 
+
+// Stand-alone M-step: totals staged in shared memory first (one parallel
+// round trip), then mstep_body.
+__global__ void __launch_bounds__(256) mstep_kernel(const loghmm_model_t* __restrict__ min_,
+                                                    const double* __restrict__ tot, int64_t width1,
+                                                    int64_t nseq, double eps, double nu_ceiling,
+                                                    double nu_tol, int max_newton,
+                                                    loghmm_model_t* __restrict__ mout,
+                                                    int32_t* __restrict__ status,
+                                                    double* __restrict__ guard, double var_ratio) {
+  extern __shared__ double tot_s[];
+  (void)width1;
+  const int Km = min_->K;
+  const int64_t w1 = (int64_t)Km * Km + 2 * Km + 2 * Km * LOGHMM_NSLOT + 1;
+  for (int64_t c = threadIdx.x; c < w1; c += blockDim.x) tot_s[c] = tot[c];
+  __syncthreads();
+  mstep_body(min_, tot_s, nseq, eps, nu_ceiling, nu_tol, max_newton, mout, status, guard, var_ratio,
+             threadIdx.x, blockDim.x);
+}
+
+// Fused statistics reduction + M-step (single rank).  Block r sums rows
+// [r*rpb, (r+1)*rpb) of the per-sequence partials column-wise (coalesced
+// rows, fixed order) into part[r]; the last block to finish sums the block
+// partials in block order into totals (also kept in shared memory) and runs
+// the M-step.  `counter` must be zero before the first launch; the last block
+// resets it.
+__global__ void __launch_bounds__(256) reduce_mstep_kernel(
+    const double* __restrict__ partials, const double* __restrict__ ll, int64_t B, int64_t width,
+    double* __restrict__ part, unsigned* __restrict__ counter, double* __restrict__ totals,
+    const loghmm_model_t* __restrict__ min_, int64_t nseq, double eps, double nu_ceiling,
+    double nu_tol, int max_newton, loghmm_model_t* __restrict__ mout, int32_t* __restrict__ status,
+    double* __restrict__ guard, double var_ratio, int do_mstep) {
+  extern __shared__ double tot_s[];
+  __shared__ bool last;
+  const int64_t W1 = width + 1;
+  const int64_t rpb = (B + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(B, r0 + rpb);
+  for (int64_t c = threadIdx.x; c < W1; c += blockDim.x) {
+    double acc = 0.0;
+    if (c < width) {
+      for (int64_t r = r0; r < r1; ++r) acc += partials[r * width + c];
+    } else {
+      for (int64_t r = r0; r < r1; ++r) acc += ll[r];
+    }
+    part[(int64_t)blockIdx.x * W1 + c] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int64_t c = threadIdx.x; c < W1; c += blockDim.x) {
+    double acc = 0.0;
+    for (unsigned r = 0; r < gridDim.x; ++r) acc += __ldcg(part + (int64_t)r * W1 + c);
+    totals[c] = acc;
+    tot_s[c] = acc;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+  __syncthreads();
+  if (do_mstep)
+    mstep_body(min_, tot_s, nseq, eps, nu_ceiling, nu_tol, max_newton, mout, status, guard,
+               var_ratio, threadIdx.x, blockDim.x);
+}
+
 // Guard pass: for every active Student-t state j (stream `sidx`), partial sums
 // over observations of w * log1p(z^2 / nu_k) for nu_k in the candidate list
 // (k = 0 is the base nu0), z = (y - mu)/sigma at the new location/scale.
@@ -537,14 +597,56 @@ __global__ void guard_select_kernel(loghmm_model_t* __restrict__ mout, int K, in
 // variance; :1051 sigma^2 = sum w u (y - mu)^2 / n): per-block partial sums of
 // w (y - centre)^2 (Gaussian, Gamma) or w u (y - centre)^2 with u at the old
 // Student-t parameters.  Blocks skip states that are not flagged.
+// Finish for state j (one thread): the exact second-pass sum S.
+__device__ inline void variance_finish_state(loghmm_model_t* __restrict__ mout, int K, int sidx,
+                                             int j, const double* __restrict__ guard, double S,
+                                             int32_t* __restrict__ status) {
+  const double* gs = guard + (size_t)(sidx * K + j) * kGuardStride;
+  loghmm_emission_t& e = mout->em[sidx][j];
+  const double n = gs[13];
+  int32_t& st = status[sidx * K + j];
+  if (e.family == LOGHMM_FAM_GAUSSIAN) {
+    e.p[0] = gs[9];
+    e.p[1] = fmax(sqrt(S / n), kScaleFloor);
+  } else if (e.family == LOGHMM_FAM_GAMMA) {
+    st = gamma_fit(n, gs[9], S / n, gs[14], e);
+    if (st >= 16) return;
+  } else if (e.family == LOGHMM_FAM_STUDENT_T) {
+    const double sigma = fmax(sqrt(S / n), kScaleFloor);
+    e.p[1] = sigma;
+    // the guard pass reads sigma from its own scratch
+    const_cast<double*>(gs)[1] = sigma;
+  }
+  em_constants(e);
+}
+
+// Exact second pass for flagged states (distributions.py:616-620 two-pass
+// variance; :1051 sigma^2 = sum w u (y - mu)^2 / n): per-block partial sums of
+// w (y - centre)^2 (Gaussian, Gamma) or w u (y - centre)^2 with u at the old
+// Student-t parameters; the last block to finish sums the block partials in
+// block order and finishes the flagged states.  Blocks exit at once when no
+// state of the stream is flagged.  `counter` must be zero before the first
+// launch; the last block resets it.
 template <typename R>
 __global__ void __launch_bounds__(256) variance_pass_kernel(const R* __restrict__ y,
                                                             const R* __restrict__ gamma, int64_t N,
                                                             int K, int sidx,
-                                                            const loghmm_model_t* __restrict__ mout,
+                                                            loghmm_model_t* __restrict__ mout,
                                                             const double* __restrict__ guard,
-                                                            double* __restrict__ part) {
+                                                            double* __restrict__ part,
+                                                            unsigned* __restrict__ counter,
+                                                            int32_t* __restrict__ status) {
   __shared__ double red[256];
+  __shared__ bool last;
+  __shared__ unsigned flagged;
+  if (threadIdx.x == 0) {
+    unsigned m = 0;
+    for (int j = 0; j < K; ++j)
+      if (guard[(size_t)(sidx * K + j) * kGuardStride + 8] != 0.0) m |= 1u << (j & 31);
+    flagged = m;
+  }
+  __syncthreads();
+  if (flagged == 0u) return;
   for (int j = 0; j < K; ++j) {
     const double* gs = guard + (size_t)(sidx * K + j) * kGuardStride;
     if (gs[8] == 0.0) continue;
@@ -574,34 +676,19 @@ __global__ void __launch_bounds__(256) variance_pass_kernel(const R* __restrict_
     if (threadIdx.x == 0) part[(size_t)blockIdx.x * K + j] = red[0];
     __syncthreads();
   }
-}
-
-__global__ void variance_finish_kernel(loghmm_model_t* __restrict__ mout, int K, int sidx,
-                                       const double* __restrict__ guard,
-                                       const double* __restrict__ part, int nblocks,
-                                       int32_t* __restrict__ status) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   const int j = threadIdx.x;
-  if (j >= K) return;
-  const double* gs = guard + (size_t)(sidx * K + j) * kGuardStride;
-  if (gs[8] == 0.0) return;
-  double S = 0.0;
-  for (int blk = 0; blk < nblocks; ++blk) S += part[(size_t)blk * K + j];
-  loghmm_emission_t& e = mout->em[sidx][j];
-  const double n = gs[13];
-  int32_t& st = status[sidx * K + j];
-  if (e.family == LOGHMM_FAM_GAUSSIAN) {
-    e.p[0] = gs[9];
-    e.p[1] = fmax(sqrt(S / n), kScaleFloor);
-  } else if (e.family == LOGHMM_FAM_GAMMA) {
-    st = gamma_fit(n, gs[9], S / n, gs[14], e);
-    if (st >= 16) return;
-  } else if (e.family == LOGHMM_FAM_STUDENT_T) {
-    const double sigma = fmax(sqrt(S / n), kScaleFloor);
-    e.p[1] = sigma;
-    // the guard pass reads sigma from its own scratch
-    const_cast<double*>(gs)[1] = sigma;
+  if (j < K && guard[(size_t)(sidx * K + j) * kGuardStride + 8] != 0.0) {
+    double S = 0.0;
+    for (unsigned blk = 0; blk < gridDim.x; ++blk) S += __ldcg(part + (size_t)blk * K + j);
+    variance_finish_state(mout, K, sidx, j, guard, S, status);
   }
-  em_constants(e);
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 }  // namespace lhmm

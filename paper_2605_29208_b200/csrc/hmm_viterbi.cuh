@@ -74,25 +74,28 @@ struct ArgMax {
   }
 };
 
-// As ArgMax, with the winning index delivered as NP predicate bits (bit p of
-// the index), which feed the bit-plane ballots directly.
+// As ArgMax, with the winning index delivered directly as the warp's NP
+// bit-plane masks: every internal node of the tree contributes one ballot of
+// its decision, and bit p of the index is selected down the tree with
+// warp-uniform LOP3s (leaf index bits fold to constants).  K-1 ballots in
+// total, no per-lane index arithmetic.
 template <typename R, int LO, int HI, int NP>
 struct ArgMaxB {
-  static __device__ __forceinline__ void run(const R* c, R& v, bool (&bits)[NP > 0 ? NP : 1]) {
+  static __device__ __forceinline__ void run(const R* c, R& v, unsigned (&m)[NP > 0 ? NP : 1]) {
     if constexpr (HI - LO == 1) {
       v = c[LO];
 #pragma unroll
-      for (int p = 0; p < (NP > 0 ? NP : 1); ++p) bits[p] = (LO >> p) & 1;
+      for (int p = 0; p < (NP > 0 ? NP : 1); ++p) m[p] = ((LO >> p) & 1) ? 0xFFFFFFFFu : 0u;
     } else {
       constexpr int MID = LO + (HI - LO + 1) / 2;
       R lv, rv;
-      bool lb[NP > 0 ? NP : 1], rb[NP > 0 ? NP : 1];
-      ArgMaxB<R, LO, MID, NP>::run(c, lv, lb);
-      ArgMaxB<R, MID, HI, NP>::run(c, rv, rb);
-      const bool right = rv > lv;
+      unsigned lm[NP > 0 ? NP : 1], rm[NP > 0 ? NP : 1];
+      ArgMaxB<R, LO, MID, NP>::run(c, lv, lm);
+      ArgMaxB<R, MID, HI, NP>::run(c, rv, rm);
+      const unsigned bt = NP > 0 ? __ballot_sync(kFull, rv > lv) : 0u;
       v = fmax(lv, rv);
 #pragma unroll
-      for (int p = 0; p < (NP > 0 ? NP : 1); ++p) bits[p] = right ? rb[p] : lb[p];
+      for (int p = 0; p < (NP > 0 ? NP : 1); ++p) m[p] = (bt & rm[p]) | (~bt & lm[p]);
     }
   }
 };
@@ -207,21 +210,18 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
 
   // One recursion step.  Every lane executes it (no divergence around the
   // shuffles / ballots); lanes past their sequence end keep their score.  The
-  // winning index leaves the argmax tree as predicate bits, one ballot per bit
-  // gives the step's bit-planes, lane 0 stores them.
+  // argmax tree returns the step's bit-planes directly (one ballot per tree
+  // decision), lane 0 stores them.
   auto step = [&](int t, R lb, bool act) {
     R cand[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) cand[i] = N::add(__shfl_sync(kFull, delta, g * K + i), la[i]);
     R best;
-    bool bits[NPa];
-    ArgMaxB<R, 0, K, NP>::run(cand, best, bits);
+    unsigned w[NPa];
+    ArgMaxB<R, 0, K, NP>::run(cand, best, w);
     const R nd = N::add(best, lb);
     delta = act ? nd : delta;
     if constexpr (NP > 0) {
-      unsigned w[NPa];
-#pragma unroll
-      for (int p = 0; p < NP; ++p) w[p] = __ballot_sync(kFull, bits[p]);
       if (lane == 0) {
         if constexpr (NP == 1) {
           planes[(size_t)t * kStepWords] = w[0];

@@ -1,4 +1,5 @@
 // Explicit instantiation: VIT kernels for dtype float, K=3.
+#define LHMM_ONLY_VIT
 #include "hmm_launch.cuh"
 namespace lhmm {
 LHMM_INST_VIT(float, 3)

@@ -1,4 +1,5 @@
 // Explicit instantiation: FBM kernels for dtype float, K=6.
+#define LHMM_ONLY_FBM
 #include "hmm_launch.cuh"
 namespace lhmm {
 LHMM_INST_FBM(float, 6)

@@ -264,7 +264,9 @@ class Workspace:
         if nbytes == 0:
             return 0, 0
         if self._buf is None or self._buf.numel() < nbytes or self._buf.device != device:
-            self._buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            # zero-filled once: the reduction / variance passes keep their
+            # inter-block counters here and leave them at zero
+            self._buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
         return int(self._buf.data_ptr()), int(self._buf.numel())
 
 
@@ -352,6 +354,31 @@ def reduce_stats(partials: torch.Tensor, ll: torch.Tensor, out: torch.Tensor | N
     check(L.loghmm_reduce_stats(_ptr(partials), _ptr(ll), B, width, _ptr(out), _stream()),
           "loghmm_reduce_stats")
     return out
+
+
+_WS_RED = Workspace()
+
+
+def reduce_mstep(partials: torch.Tensor, ll: torch.Tensor, totals: torch.Tensor,
+                 dm_in: DeviceModel | None = None, n_sequences: int = 0, config=None,
+                 dm_out: DeviceModel | None = None, status: torch.Tensor | None = None,
+                 guard: torch.Tensor | None = None, td: torch.dtype = torch.float64,
+                 workspace: Workspace | None = None) -> torch.Tensor:
+    """Fused single-rank reduction + M-step (reduction only when dm_in is None)."""
+    L = lib()
+    B, width = partials.shape
+    ws = workspace if workspace is not None else _WS_RED
+    wptr, wlen = ws.get(int(L.loghmm_reduce_workspace_bytes(B, width)), partials.device)
+    if dm_in is None:
+        args = (None, 0, 0.0, 0.0, 0.0, 0, 0.0, None, None, None)
+    else:
+        e = config.ecme
+        args = (dm_in.ptr(), n_sequences, float(config.collapse_epsilon), float(e.nu_ceiling),
+                float(e.nu_tol), int(e.max_newton), var_ratio(td), dm_out.ptr(), _ptr(status),
+                _ptr(guard))
+    check(L.loghmm_reduce_mstep(_ptr(partials), _ptr(ll), B, width, _ptr(totals), *args, wptr, wlen,
+                                _stream()), "loghmm_reduce_mstep")
+    return totals
 
 
 GUARD_STRIDE = 16  # doubles of scratch per (stream, state)

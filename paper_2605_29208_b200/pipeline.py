@@ -13,6 +13,8 @@ results (total log-likelihood, the updated model block) like a user would.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -24,7 +26,7 @@ __all__ = ["Pipeline"]
 
 
 class Pipeline:
-    KERNELS_PER_RUN = 4  # fb, viterbi, reduce, mstep (+1 guard pass per Student-t stream)
+    KERNELS_PER_RUN = 3  # fb, viterbi, fused reduce+mstep (single rank)
 
     def __init__(self, model: HmmModel, B: int, T: int, dtype="float32", *, outputs=True,
                  config: TrainingConfig | None = None, process_group=None):
@@ -67,6 +69,7 @@ class Pipeline:
         self.need_more = torch.zeros(1, dtype=torch.int32, device=dev)
         self.ws_fb = engine.Workspace()
         self.ws_vit = engine.Workspace()
+        self.ws_red = engine.Workspace()
         self.s_fb = torch.cuda.Stream(device=dev)
         self.s_vit = torch.cuda.Stream(device=dev)
         fams = self.dm.host["em"]["family"]
@@ -81,8 +84,8 @@ class Pipeline:
 
     @property
     def kernels_per_run(self) -> int:
-        # + variance pass & finish per variance stream, + guard & select per Student-t stream
-        return self.KERNELS_PER_RUN + 2 * len(self.var_streams) + 2 * len(self.student_streams)
+        # + one variance pass per variance stream, + guard & select per Student-t stream
+        return self.KERNELS_PER_RUN + len(self.var_streams) + 2 * len(self.student_streams)
 
     def load(self, y) -> None:
         """Copy observations [B, T] (or [B, T, 2]) into the device batch."""
@@ -97,30 +100,53 @@ class Pipeline:
         main = torch.cuda.current_stream(self.dev)
         self.s_fb.wait_stream(main)
         self.s_vit.wait_stream(main)
-        # Viterbi first: its grid is one partial wave (one CTA per SM), so the
-        # forward-backward CTAs queued after it fill the remaining SM slots and
-        # the two kernels run concurrently.
-        with torch.cuda.stream(self.s_vit):
-            if time_kernels:
-                self.ev["vit"][0].record(self.s_vit)
-            engine.viterbi(self.batch, self.dm, out=self.vit, workspace=self.ws_vit)
-            if time_kernels:
-                self.ev["vit"][1].record(self.s_vit)
-        with torch.cuda.stream(self.s_fb):
-            if time_kernels:
-                self.ev["fb"][0].record(self.s_fb)
-            engine.forward_backward(self.batch, self.dm, stats=True, out=self.fb, workspace=self.ws_fb)
-            if time_kernels:
-                self.ev["fb"][1].record(self.s_fb)
+        # Viterbi first by default: its grid is one partial wave (one CTA per
+        # SM), so the forward-backward CTAs queued after it fill the remaining
+        # SM slots and the two kernels run concurrently.
+        # LOGHMM_PIPE_ORDER=fb_first | serial reorders them (measurement aid).
+        order = os.environ.get("LOGHMM_PIPE_ORDER", "vit_first")
+
+        def launch_vit():
+            with torch.cuda.stream(self.s_vit):
+                if time_kernels:
+                    self.ev["vit"][0].record(self.s_vit)
+                engine.viterbi(self.batch, self.dm, out=self.vit, workspace=self.ws_vit)
+                if time_kernels:
+                    self.ev["vit"][1].record(self.s_vit)
+
+        def launch_fb():
+            with torch.cuda.stream(self.s_fb):
+                if time_kernels:
+                    self.ev["fb"][0].record(self.s_fb)
+                engine.forward_backward(self.batch, self.dm, stats=True, out=self.fb,
+                                        workspace=self.ws_fb)
+                if time_kernels:
+                    self.ev["fb"][1].record(self.s_fb)
+
+        if order == "fb_first":
+            launch_fb()
+            launch_vit()
+        elif order == "serial":
+            launch_vit()
+            self.s_fb.wait_stream(self.s_vit)
+            launch_fb()
+        else:
+            launch_vit()
+            launch_fb()
         main.wait_stream(self.s_fb)
         main.wait_stream(self.s_vit)
-        engine.reduce_stats(self.fb.partials, self.fb.ll, self.totals)
-        if self.pg is not None:
+        if self.pg is None:
+            # single rank: block reduction and M-step in one launch
+            engine.reduce_mstep(self.fb.partials, self.fb.ll, self.totals, self.dm, self.B,
+                                self.config, self.dm_next, self.status, self.guard, self.td,
+                                workspace=self.ws_red)
+        else:
             import torch.distributed as dist
 
+            engine.reduce_mstep(self.fb.partials, self.fb.ll, self.totals, workspace=self.ws_red)
             dist.all_reduce(self.totals, group=self.pg)
-        engine.mstep(self.dm, self.totals, self.B * (1 if self.pg is None else self._world()),
-                     self.config, self.dm_next, self.status, self.guard, self.td)
+            engine.mstep(self.dm, self.totals, self.B * self._world(), self.config, self.dm_next,
+                         self.status, self.guard, self.td)
         for s in self.var_streams:
             engine.variance_pass(self.batch, self.dm_next, self.fb.gamma, s, self.guard, self.status)
         for s in self.student_streams:

@@ -2,7 +2,7 @@
 """Per-kernel timing of the config-2 hot path, each kernel launched alone
 (CUDA events on the launching stream, L2 flushed between launches).
 
-  python tools/prof_kernels.py [--dtype float32] [--reps 20] [--only fb|vit]
+  python tools/prof_kernels.py [--dtype float32] [--reps 20] [--only fb|vit|small]
 """
 
 import argparse
@@ -55,6 +55,23 @@ def main():
             lambda: engine.forward_backward(batch, dm, alpha=False, beta=False, gamma=False), a.reps, flush)
     if a.only in ("", "vit"):
         out["vit_ms"] = timeit(lambda: engine.viterbi(batch, dm, out=vo), a.reps, flush)
+    if a.only in ("", "small"):
+        from paper_2605_29208_b200.training import TrainingConfig
+        tc = TrainingConfig()
+        tot = torch.empty(fbo.partials.shape[1] + 1, dtype=torch.float64, device="cuda")
+        dm2 = engine.DeviceModel.from_model(cfg.init)
+        st = torch.zeros(2 * dm.K, dtype=torch.int32, device="cuda")
+        gd = torch.zeros(2 * dm.K * engine.GUARD_STRIDE, dtype=torch.float64, device="cuda")
+        ws = engine.Workspace()
+        out["reduce_stats_ms"] = timeit(lambda: engine.reduce_stats(fbo.partials, fbo.ll, tot), a.reps, flush)
+        out["reduce_only_ms"] = timeit(
+            lambda: engine.reduce_mstep(fbo.partials, fbo.ll, tot, workspace=ws), a.reps, flush)
+        out["reduce_mstep_ms"] = timeit(
+            lambda: engine.reduce_mstep(fbo.partials, fbo.ll, tot, dm, a.B, tc, dm2, st, gd,
+                                        workspace=ws), a.reps, flush)
+        out["mstep_ms"] = timeit(lambda: engine.mstep(dm, tot, a.B, tc, dm2, st, gd), a.reps, flush)
+        out["variance_pass_ms"] = timeit(
+            lambda: engine.variance_pass(batch, dm2, fbo.gamma, 0, gd, st), a.reps, flush)
     esz = 4 if a.dtype == "float32" else 8
     K = 4
     if "fb_ms" in out:
