@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <climits>
 
 #include "hmm_large.cuh"
 #include "hmm_launch.cuh"
@@ -174,31 +175,66 @@ static cudaError_t dispatch_vit_small(int K, const VitArgs& a, int cfg, bool gl,
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// Forward-backward decomposition: chunked scan over T (hmm_fb.cuh) by
-// default; meet-in-the-middle (hmm_fbm.cuh) on request.
-// LOGHMM_FB_ALGO=chunked|mitm forces one (tests exercise both).
-static bool use_mitm(int K, int64_t B) {
-  if (K > 8 || K < 2) return false;
-  const char* env = getenv("LOGHMM_FB_ALGO");
-  if (env && strcmp(env, "chunked") == 0) return false;
-  if (env && strcmp(env, "mitm") == 0) return true;
-  // the chunked scan is currently faster at every measured shape (see
-  // profiles/); the meet-in-the-middle kernel is kept behind the switch
-  return false;
+// Forward-backward decomposition.  Equal-length batches whose length splits
+// into <= 32 chunks of a multiple-of-8 length take the chunk-operator +
+// meet-in-the-middle kernel (hmm_fbc.cuh); everything else (ragged batches,
+// per-step xi output, long sequences, K = 1) takes the chunked scan
+// (hmm_fb.cuh).  LOGHMM_FB_ALGO=chunked forces the latter (tests exercise both).
+static int fbc_chunk_len(int64_t T) {
+  if (T < 8) return 0;
+  int64_t L = (T + kWarp - 1) / kWarp;
+  L = (L + 7) / 8 * 8;
+  for (; L <= T; L += 8)
+    if (T % L == 0) return (int)L;
+  return 0;
 }
 
-static int64_t mitm_kp(int K) { return K >= 2 ? 2 * ((K + 1) / 2) : K; }
+static int fbc_warp_elems(int K, int esz, int L) {
+#define C_(KK) case KK: return esz == 8 ? fb_chunk_warp_elems<double, KK>(L) : fb_chunk_warp_elems<float, KK>(L);
+  switch (K) { C_(2) C_(3) C_(4) C_(5) C_(6) C_(7) C_(8) default: return 0; }
+#undef C_
+}
+
+// tensor-memory columns for the fp32 park: L steps x KP (K padded to 1,2,4,8)
+static int fbc_tm_cols(int K, int L) {
+  const int kp = K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : 8;
+  int n = 32;
+  while (n < L * kp) n <<= 1;
+  return n;
+}
+
+constexpr int kFbcWarpsPerBlock = 4;  // one warpgroup (kFbcWarps)
+constexpr size_t kFbcMaxWarpBytes = 100 * 1024;
+
+static bool use_fbc(int K, int64_t B, int64_t N, int64_t max_T, int esz, bool xi, int* L_out,
+                    size_t* warp_bytes) {
+  const char* env = getenv("LOGHMM_FB_ALGO");
+  if (env && strcmp(env, "chunked") == 0) return false;
+  // fp64 stays on the chunked scan until its exp2/log2 are cheaper than
+  // libm's (the re-sweep evaluates them once more per step than the scan)
+  if (esz != 4) return false;
+  if (K < 2 || K > 8 || xi || max_T < 8 || N != B * max_T || max_T > INT32_MAX) return false;
+  const int L = fbc_chunk_len(max_T);
+  if (L == 0) return false;
+  const size_t wb = (size_t)fbc_warp_elems(K, esz, L) * esz;
+  if (wb > kFbcMaxWarpBytes) return false;
+  if (esz == 4 && fbc_tm_cols(K, L) > 256) return false;  // tensor-memory park
+  *L_out = L;
+  *warp_bytes = wb;
+  return true;
+}
 
 template <typename R>
-static cudaError_t dispatch_fb_mitm(int K, const FBMArgs& a, int cfg, dim3 grid, cudaStream_t st) {
+static cudaError_t dispatch_fb_chunk(int K, const FBCArgs& a, int cfg, dim3 grid, dim3 block,
+                                     size_t smem, cudaStream_t st) {
   switch (K) {
-    case 2: return launch_fb_mitm<R, 2>(a, cfg, grid, fb_mitm_smem<R, 2>(), st);
-    case 3: return launch_fb_mitm<R, 3>(a, cfg, grid, fb_mitm_smem<R, 3>(), st);
-    case 4: return launch_fb_mitm<R, 4>(a, cfg, grid, fb_mitm_smem<R, 4>(), st);
-    case 5: return launch_fb_mitm<R, 5>(a, cfg, grid, fb_mitm_smem<R, 5>(), st);
-    case 6: return launch_fb_mitm<R, 6>(a, cfg, grid, fb_mitm_smem<R, 6>(), st);
-    case 7: return launch_fb_mitm<R, 7>(a, cfg, grid, fb_mitm_smem<R, 7>(), st);
-    default: return launch_fb_mitm<R, 8>(a, cfg, grid, fb_mitm_smem<R, 8>(), st);
+    case 2: return launch_fb_chunk<R, 2>(a, cfg, grid, block, smem, st);
+    case 3: return launch_fb_chunk<R, 3>(a, cfg, grid, block, smem, st);
+    case 4: return launch_fb_chunk<R, 4>(a, cfg, grid, block, smem, st);
+    case 5: return launch_fb_chunk<R, 5>(a, cfg, grid, block, smem, st);
+    case 6: return launch_fb_chunk<R, 6>(a, cfg, grid, block, smem, st);
+    case 7: return launch_fb_chunk<R, 7>(a, cfg, grid, block, smem, st);
+    default: return launch_fb_chunk<R, 8>(a, cfg, grid, block, smem, st);
   }
 }
 
@@ -221,11 +257,6 @@ size_t loghmm_fb_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N,
   (void)B;
   const int esz = dtype == LOGHMM_F64 ? 8 : 4;
   if (K > 8) return align256((size_t)N * K * esz);
-  if (use_mitm(K, B)) {
-    const int64_t G = 16;
-    const int64_t Bp = ((B + G - 1) / G) * G;
-    return align256((size_t)max_T * Bp * mitm_kp(K) * esz);
-  }
   FBGeom g = fb_geom(K, esz, 2, max_T);
   return align256((size_t)B * g.Lmax * kWarp * K * esz);
 }
@@ -299,31 +330,35 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
   const int cfg = cfg_of(h_desc, &fams);
   a.stream_fams = fams;
   cudaError_t e;
-  if (use_mitm(K, B)) {
-    FBMArgs m{};
-    m.model = model;
-    m.y0 = a.y0;
-    m.y1 = a.y1;
-    m.offsets = offsets;
-    m.B = B;
-    m.lut = lgamma_lut;
-    m.lut_n = lut_n;
-    m.n_streams = a.n_streams;
-    m.log_alpha = log_alpha;
-    m.log_beta = log_beta;
-    m.gamma = gamma;
-    m.xi = xi;
-    m.ll = ll;
-    m.partials = partials;
-    m.flags = flags;
-    m.ws = workspace;
-    const int64_t G = 16;
-    const int64_t nblk = (B + G - 1) / G;
-    m.ws_bstride = nblk * G * mitm_kp(K);
-    m.stats_width = a.stats_width;
-    dim3 grid((unsigned)nblk);
-    e = dtype == LOGHMM_F64 ? dispatch_fb_mitm<double>(K, m, cfg, grid, st)
-                            : dispatch_fb_mitm<float>(K, m, cfg, grid, st);
+  int fbcL = 0;
+  size_t fbcW = 0;
+  if (use_fbc(K, B, N, max_T, esz, xi != nullptr, &fbcL, &fbcW)) {
+    FBCArgs c{};
+    c.model = model;
+    c.y0 = a.y0;
+    c.y1 = a.y1;
+    c.B = B;
+    c.T = (int)max_T;
+    c.L = fbcL;
+    c.lut = lgamma_lut;
+    c.lut_n = lut_n;
+    c.n_streams = a.n_streams;
+    c.stream_fams = fams;
+    c.log_alpha = log_alpha;
+    c.log_beta = log_beta;
+    c.gamma = gamma;
+    c.ll = ll;
+    c.partials = partials;
+    c.flags = flags;
+    c.stats_width = a.stats_width;
+    c.tm_cols = esz == 4 ? fbc_tm_cols(K, fbcL) : 0;
+    // fp32: one warpgroup per CTA (tensor-memory lane quadrants); fp64: as
+    // many warps as the shared-memory park allows, up to four
+    const int wpb = esz == 4 ? kFbcWarpsPerBlock
+                             : (int)std::max<size_t>(1, std::min<size_t>(kFbcWarpsPerBlock, (220 * 1024) / fbcW));
+    dim3 grid((unsigned)((B + wpb - 1) / wpb)), block(32 * wpb);
+    e = dtype == LOGHMM_F64 ? dispatch_fb_chunk<double>(K, c, cfg, grid, block, fbcW * wpb, st)
+                            : dispatch_fb_chunk<float>(K, c, cfg, grid, block, fbcW * wpb, st);
   } else if (K <= 8) {
     FBGeom g = fb_geom(K, esz, h_desc->n_streams, max_T);
     a.L_align = g.L_align;

@@ -1,0 +1,916 @@
+// hmm_fbc.cuh — batched forward-backward for equal-length sequences, K <= 8:
+// chunk operators + scan, then a meet-in-the-middle re-sweep inside each chunk.
+//
+// Same outputs and statistics as hmm_fb.cuh (inference.py:129-188,
+// training.py:187-210); this is the decomposition used for [B, T] batches
+// whose length splits into C <= 32 chunks of L steps (L a multiple of 8).
+//
+//   pass 1  one warp per sequence, lane c owns chunk [cL, cL+L): it builds the
+//           chunk transfer operator M_c = prod A diag(b_t) (linear, power-of-two
+//           normalised, log2 offset), K^3 FMA per step, nothing stored.
+//   scan    Hillis-Steele over the lanes (shuffles) gives each lane its entering
+//           forward vector alpha~_{cL-1}, its exiting backward vector
+//           beta~_{cL+L-1} and the sequence log-likelihood.
+//   pass 2  each lane runs the forward recursion up its chunk and the backward
+//           recursion down it IN THE SAME LOOP (two independent dependency
+//           chains per iteration).  In the first half each direction parks its
+//           normalised vector in shared memory; in the second half each one
+//           meets the other's parked vectors and forms gamma, the xi totals and
+//           the family statistics on the fly.  Every emission is evaluated once
+//           per direction; no vector ever leaves the SM.
+//
+// Outputs (log_alpha, log_beta, gamma) are staged per lane as 4-step slabs in
+// shared memory and written by the whole warp as 16-byte coalesced units.
+// All recursions run in log2 units (MUFU ex2/lg2); carried state is a linear
+// vector plus a log2 offset, which keeps fp32 relative precision (SURVEY.md
+// §7.3-2).  The Gaussian emission is two FMAs per state in that form.
+#pragma once
+
+#include <type_traits>
+
+#include "hmm_fb.cuh"
+
+namespace lhmm {
+
+struct FBCArgs {
+  const loghmm_model_t* model;
+  const void* y0;
+  const void* y1;
+  int64_t B;
+  int T;  // common sequence length, T = C * L
+  int L;  // chunk length, multiple of 8
+  const double* lut;
+  int lut_n;
+  int n_streams;
+  int stream_fams;
+  void* log_alpha;
+  void* log_beta;
+  void* gamma;
+  double* ll;
+  double* partials;
+  int64_t* flags;
+  int64_t stats_width;
+  int tm_cols;  // tensor-memory columns per CTA (fp32 park)
+};
+
+template <typename R, int K>
+struct FBCGeom {
+  static constexpr int VB = K * (int)sizeof(R);  // bytes of one state vector
+  static constexpr int ROWB = 4 * VB;            // one lane's 4-step slab (multiple of 16)
+  static constexpr int PITCHB = ((ROWB / 16) % 2 == 0) ? ROWB + 16 : ROWB;
+  static constexpr int PITCH = PITCHB / (int)sizeof(R);  // elements
+  static constexpr int STAGE = kWarp * PITCH;             // one output stream
+  static constexpr int U = ROWB / 16;                     // 16-byte units per slab row
+  static constexpr int EPU = 16 / (int)sizeof(R);         // elements per unit
+  // shared-memory elements per warp: four output stages, plus the parked
+  // vectors [L][32][K] for fp64 (fp32 parks them in tensor memory)
+  static __host__ __device__ int warp_elems(int L) {
+    return 4 * STAGE + (sizeof(R) == 4 ? 0 : L * kWarp * K);
+  }
+};
+
+// K-vector shared-memory store / load with the widest aligned access.
+template <typename R, int K>
+struct SVec {
+  static __device__ __forceinline__ void st(R* p, const R (&v)[K]) {
+    if constexpr (sizeof(R) == 4 && K % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < K; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else if constexpr (K % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < K; i += 2) {
+        if constexpr (sizeof(R) == 4) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
+        else *reinterpret_cast<double2*>(p + i) = make_double2(v[i], v[i + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < K; ++i) p[i] = v[i];
+    }
+  }
+  static __device__ __forceinline__ void ld(const R* p, R (&v)[K]) {
+    if constexpr (sizeof(R) == 4 && K % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < K; i += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(p + i);
+        v[i] = q.x; v[i + 1] = q.y; v[i + 2] = q.z; v[i + 3] = q.w;
+      }
+    } else if constexpr (K % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < K; i += 2) {
+        if constexpr (sizeof(R) == 4) {
+          const float2 q = *reinterpret_cast<const float2*>(p + i);
+          v[i] = q.x; v[i + 1] = q.y;
+        } else {
+          const double2 q = *reinterpret_cast<const double2*>(p + i);
+          v[i] = q.x; v[i + 1] = q.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < K; ++i) v[i] = p[i];
+    }
+  }
+};
+
+// Four consecutive observations (16-byte aligned) in registers.
+template <typename R>
+struct Y4 {
+  R v[4];
+  __device__ __forceinline__ void load(const R* p) {
+    if constexpr (sizeof(R) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+  }
+};
+
+// Emission log2-densities of all states (u_j = log2 b_j(y)).  The Gaussian is
+// rewritten as u = c - w^2 with w = y*s - mu*s, s = sqrt(log2(e)/2)/sigma.
+template <typename R, int K, int CFG>
+struct Em2 {
+  Emit<R, K, CFG> em;
+  R ga[K], go[K], gc[K];
+  __device__ __forceinline__ void load(const loghmm_model_t* m, int n_streams, int fams,
+                                       const double* lut, int lut_n) {
+    em.load(m, n_streams, fams, lut, lut_n);
+    if constexpr (CFG == kCfgGauss) {
+      const double h = sqrt(0.5 * 1.4426950408889634);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const double s = h / m->em[0][j].p[1];
+        ga[j] = (R)s;
+        go[j] = (R)(-m->em[0][j].p[0] * s);
+        gc[j] = (R)(m->em[0][j].c[0] * 1.4426950408889634);
+      }
+    }
+  }
+  __device__ __forceinline__ void eval(R y0, R y1, ObsFeat<R>& f0, ObsFeat<R>& f1, R (&u)[K],
+                                       bool& oob) const {
+    if constexpr (CFG == kCfgGauss) {
+      f0.y = y0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const R w = fma(y0, ga[j], go[j]);
+        u[j] = fma(-w, w, gc[j]);
+      }
+    } else {
+      R lb[K];
+      em.eval(y0, y1, f0, f1, lb, oob);
+#pragma unroll
+      for (int j = 0; j < K; ++j) u[j] = lb[j] * R(1.4426950408889634);
+    }
+  }
+};
+
+// Power-of-two renormalisation of a vector, exponent added to a log2 offset
+// kept in R (sums of small integers: exact).
+template <typename R, int K>
+__device__ __forceinline__ void renorm_vec(R (&v)[K], R& off) {
+  R m = v[0];
+#pragma unroll
+  for (int i = 1; i < K; ++i) m = rmax(m, v[i]);
+  if (m > R(0)) {
+    int e;
+    const R s = Num<R>::pow2_scale(m, e);
+    off += (R)e;
+#pragma unroll
+    for (int i = 0; i < K; ++i) v[i] *= s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor memory as per-warp scratch for the parked vectors (fp32).  A CTA is
+// one warpgroup (4 warps); warp w owns TMEM lanes [32w, 32w+32) and, in them,
+// one column block of KP columns per parked step.  tcgen05.st / tcgen05.ld
+// with the 32x32b shape move one 32-bit column per lane per repetition.
+// ---------------------------------------------------------------------------
+template <int K>
+struct KPad {
+  static constexpr int V = K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : 8;
+};
+
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[1]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(a), "r"(r[0]) : "memory");
+}
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[2]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "r"(r[0]), "r"(r[1])
+               : "memory");
+}
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(a),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[1]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[0]) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[2]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(a)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(a)
+               : "memory");
+}
+// Wait for this thread's outstanding tcgen05.ld; the registers are operands
+// so no use of them can be scheduled above the wait.
+template <int N>
+__device__ __forceinline__ void tm_wait_ld(uint32_t (&x)[N], uint32_t (&y)[N]) {
+  if constexpr (N == 1) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(x[0]), "+r"(y[0])::"memory");
+  } else if constexpr (N == 2) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(x[0]), "+r"(x[1]), "+r"(y[0]), "+r"(y[1])::"memory");
+  } else if constexpr (N == 4) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(y[0]), "+r"(y[1]), "+r"(y[2]),
+                   "+r"(y[3])::"memory");
+  } else {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]),
+                   "+r"(x[7]), "+r"(y[0]), "+r"(y[1]), "+r"(y[2]), "+r"(y[3]), "+r"(y[4]), "+r"(y[5]),
+                   "+r"(y[6]), "+r"(y[7])::"memory");
+  }
+}
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+constexpr int kFbcWarps = 4;  // warps (sequences) per CTA: one warpgroup
+
+template <typename R, int K, int CFG>
+__global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
+  typedef Num<R> N;
+  typedef CfgTraits<CFG> TR;
+  typedef FBCGeom<R, K> G;
+  constexpr bool kTwo = (CFG == kCfgGammaVM || CFG == kCfgMixed);
+  constexpr bool TM = sizeof(R) == 4;  // park in tensor memory (fp32) or shared memory (fp64)
+  constexpr int KP = KPad<K>::V;
+  constexpr R kLN2 = R(0.6931471805599453);
+  constexpr double kLN2d = 0.6931471805599453094;
+  constexpr R kFloor = sizeof(R) == 4 ? R(-1e30) : R(-1e300);  // finite stand-in for max of all -inf
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_tmem;
+
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  const bool valid = b < a.B;
+
+  uint32_t tbase = 0;
+  if constexpr (TM) {
+    if (wib == 0) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem);
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst),
+                   "r"((uint32_t)a.tm_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    tbase = s_tmem + ((uint32_t)(32 * wib) << 16);
+  }
+
+  if (valid) {
+    const int T = a.T, L = a.L, C = T / L, HL = L / 2, NG = L / 4;
+    const bool act = lane < C;
+    const int t0 = act ? lane * L : 0;
+    const int64_t start = b * (int64_t)T;
+    const bool two = kTwo && a.n_streams > 1;
+
+    R* wsm = reinterpret_cast<R*>(smem_raw) + (size_t)wib * G::warp_elems(L);
+    R* stA = wsm;              // log_alpha slabs
+    R* stB = stA + G::STAGE;   // log_beta slabs
+    R* stGf = stB + G::STAGE;  // gamma slabs, forward direction
+    R* stGb = stGf + G::STAGE; // gamma slabs, backward direction
+    R* mypark = stGb + G::STAGE + lane * K;  // fp64: [L][32][K] in shared memory
+    R* myA = stA + lane * G::PITCH;
+    R* myB = stB + lane * G::PITCH;
+    R* myGf = stGf + lane * G::PITCH;
+    R* myGb = stGb + lane * G::PITCH;
+
+    auto park_st = [&](int slot, const R (&v)[K]) {
+      if constexpr (TM) {
+        uint32_t r[KP];
+#pragma unroll
+        for (int j = 0; j < KP; ++j) r[j] = j < K ? __float_as_uint((float)v[j < K ? j : 0]) : 0u;
+        tm_st(tbase + (uint32_t)(slot * KP), r);
+      } else {
+        SVec<R, K>::st(mypark + slot * (kWarp * K), v);
+      }
+    };
+
+    // ---- model -----------------------------------------------------------
+    const loghmm_model_t* __restrict__ md = a.model;
+    R Am[K][K];
+    R minA = R(1);
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        Am[i][j] = (R)md->A[i * K + j];
+        minA = fmin(Am[i][j], minA);
+      }
+    R lpi2[K], pil[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      lpi2[j] = (R)(md->log_pi[j] * 1.4426950408889634);
+      pil[j] = (R)md->pi[j];
+    }
+    Em2<R, K, CFG> em;
+    em.load(md, a.n_streams, a.stream_fams, a.lut, a.lut_n);
+    // Renormalise every nn steps: the max entry of the operator / forward
+    // vector shrinks by at most min(A) per step (the backward vector by at
+    // most min(A)^2), so nn steps stay above 2^-100 (fp32) / 2^-900 (fp64).
+    int nn = 1, nnb = 1;
+    if (minA > R(0)) {
+      const double lg = -log2((double)minA);
+      const double budget = sizeof(R) == 4 ? 100.0 : 900.0;
+      nn = lg <= 0.0 ? 8 : (int)fmin(8.0, fmax(1.0, floor(budget / lg)));
+      nnb = lg <= 0.0 ? 8 : (int)fmin(8.0, fmax(1.0, floor(budget / (2.0 * lg))));
+    }
+    // every step (nn < 4) or every 1 / 2 four-step groups
+    const bool rn_step = nn < 4, rnb_step = nnb < 4;
+    const int rn_groups = nn >= 8 ? 2 : 1, rnb_groups = nnb >= 8 ? 2 : 1;
+
+    const R* __restrict__ y0c = reinterpret_cast<const R*>(a.y0) + start + t0;
+    const R* __restrict__ y1c = two ? reinterpret_cast<const R*>(a.y1) + start + t0 : y0c;
+
+    bool oob = false, bad = false;
+
+    // u_j = log2 b_j(y), m = max_j u_j clamped finite, bh_j = 2^(u_j - m)
+    auto emit = [&](R yv0, R yv1, ObsFeat<R>& f0, ObsFeat<R>& f1, R (&u)[K], R (&bh)[K]) -> R {
+      em.eval(yv0, yv1, f0, f1, u, oob);
+      R m = u[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) m = fmax(m, u[j]);
+      m = fmax(m, kFloor);
+#pragma unroll
+      for (int j = 0; j < K; ++j) bh[j] = N::fex2(u[j] - m);
+      return m;
+    };
+
+    // ===================== pass 1: chunk operator ===========================
+    R Mop[K][K];
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+#pragma unroll
+      for (int c = 0; c < K; ++c) Mop[r][c] = r == c ? R(1) : R(0);
+    R moff = R(0);
+    R seed_u[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) seed_u[j] = N::ninf();
+    {
+      Y4<R> yc, yc1, yn, yn1;
+      yc.load(y0c);
+      if (two) yc1.load(y1c);
+      int gcd = rn_groups;
+#pragma unroll 1
+      for (int g = 0; g < NG; ++g) {
+        if (g + 1 < NG) {
+          yn.load(y0c + 4 * (g + 1));
+          if (two) yn1.load(y1c + 4 * (g + 1));
+        }
+#pragma unroll
+        for (int sub = 0; sub < 4; ++sub) {
+          const R yv0 = yc.v[sub];
+          const R yv1 = two ? yc1.v[sub] : R(0);
+          ObsFeat<R> f0, f1;
+          R u[K], bh[K];
+          const R m = emit(yv0, yv1, f0, f1, u, bh);
+          bad |= !(m > kFloor);  // a dead step (all -inf) or NaN observation
+          R Nw[K][K];
+#pragma unroll
+          for (int r = 0; r < K; ++r)
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+              R acc = Mop[r][0] * Am[0][c];
+#pragma unroll
+              for (int i = 1; i < K; ++i) acc = fma(Mop[r][i], Am[i][c], acc);
+              Nw[r][c] = acc * bh[c];
+            }
+          if (sub == 0) {
+            // t = 0 (lane 0, first group) seeds the forward vector
+            // (log2 pi + log2 b_0): no operator step
+            const bool first = (g == 0) && (lane == 0);
+#pragma unroll
+            for (int j = 0; j < K; ++j) seed_u[j] = first ? lpi2[j] + u[j] : seed_u[j];
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+              for (int c = 0; c < K; ++c) Mop[r][c] = first ? Mop[r][c] : Nw[r][c];
+            moff += first ? R(0) : m;
+          } else {
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+              for (int c = 0; c < K; ++c) Mop[r][c] = Nw[r][c];
+            moff += m;
+          }
+          if (rn_step || (sub == 3 && --gcd == 0)) {
+            if (!rn_step) gcd = rn_groups;
+            R mx = Mop[0][0];
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+              for (int c = 0; c < K; ++c) mx = fmax(mx, Mop[r][c]);
+            if (mx > R(0)) {
+              int e;
+              const R s = N::pow2_scale(mx, e);
+              moff += (R)e;
+#pragma unroll
+              for (int r = 0; r < K; ++r)
+#pragma unroll
+                for (int c = 0; c < K; ++c) Mop[r][c] *= s;
+            }
+          }
+        }
+        yc = yn;
+        if (two) yc1 = yn1;
+      }
+    }
+    double mo = (double)moff;
+    {
+      R mx = Mop[0][0];
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) mx = fmax(mx, Mop[r][c]);
+      if (!(mx > R(0))) mo = -CUDART_INF;
+    }
+    if (!act) {
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) Mop[r][c] = r == c ? R(1) : R(0);
+      mo = 0.0;
+      bad = false;
+    }
+
+    // ===================== scan over chunks =================================
+    R a_in[K];
+    double lam_in, LL;
+    {
+      R Q[K][K];
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) Q[r][c] = Mop[r][c];
+      double qo = mo;
+#pragma unroll 1
+      for (int d = 1; d < kWarp; d <<= 1) {
+        R P[K][K];
+        double po;
+        shfl_mat<R, K>(P, po, Q, qo, d, true);
+        if (lane >= d) {
+          R Z[K][K];
+          matmul<R, K>(P, Q, Z);
+#pragma unroll
+          for (int r = 0; r < K; ++r)
+#pragma unroll
+            for (int c = 0; c < K; ++c) Q[r][c] = Z[r][c];
+          qo += po;
+          normalise_mat2<R, K>(Q, qo);
+        }
+      }
+      R sm = seed_u[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) sm = fmax(sm, seed_u[j]);
+      R sv[K];
+      const bool sfin = sm > N::ninf();
+#pragma unroll
+      for (int j = 0; j < K; ++j) sv[j] = sfin ? N::fex2(seed_u[j] - sm) : R(0);
+      double so = sfin ? (double)sm : -CUDART_INF;
+#pragma unroll
+      for (int j = 0; j < K; ++j) sv[j] = __shfl_sync(kFull, sv[j], 0);
+      so = __shfl_sync(kFull, so, 0);
+      R v[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        R acc = sv[0] * Q[0][c];
+#pragma unroll
+        for (int i = 1; i < K; ++i) acc = fma(sv[i], Q[i][c], acc);
+        v[c] = acc;
+      }
+      double vo = so + qo;
+      normalise_vec2<R, K>(v, vo);
+      R vs = v[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) vs += v[j];
+      double llv = (vo + (double)N::flg2(vs)) * kLN2d;
+      if (!(vs > R(0))) llv = -CUDART_INF;
+      LL = __shfl_sync(kFull, llv, kWarp - 1);
+#pragma unroll
+      for (int j = 0; j < K; ++j) a_in[j] = __shfl_up_sync(kFull, v[j], 1);
+      lam_in = __shfl_up_sync(kFull, vo, 1);
+    }
+    R b_ex[K];
+    double rho_ex;
+    {
+      R S[K][K];
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+#pragma unroll
+        for (int c = 0; c < K; ++c) S[r][c] = Mop[r][c];
+      double so = mo;
+#pragma unroll 1
+      for (int d = 1; d < kWarp; d <<= 1) {
+        R Y[K][K];
+        double yo;
+        shfl_mat<R, K>(Y, yo, S, so, d, false);
+        if (lane + d < kWarp) {
+          R Z[K][K];
+          matmul<R, K>(S, Y, Z);
+#pragma unroll
+          for (int r = 0; r < K; ++r)
+#pragma unroll
+            for (int c = 0; c < K; ++c) S[r][c] = Z[r][c];
+          so += yo;
+          normalise_mat2<R, K>(S, so);
+        }
+      }
+      R z[K];
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        R acc = S[r][0];
+#pragma unroll
+        for (int c = 1; c < K; ++c) acc += S[r][c];
+        z[r] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) b_ex[j] = __shfl_down_sync(kFull, z[j], 1);
+      rho_ex = __shfl_down_sync(kFull, so, 1);
+      if (lane == kWarp - 1) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) b_ex[j] = R(1);
+        rho_ex = 0.0;
+      }
+      normalise_vec2<R, K>(b_ex, rho_ex);
+    }
+
+    // ===================== pass 2: meet in the middle =======================
+    R* __restrict__ outA = reinterpret_cast<R*>(a.log_alpha);
+    R* __restrict__ outB = reinterpret_cast<R*>(a.log_beta);
+    R* __restrict__ outG = reinterpret_cast<R*>(a.gamma);
+    // flush geometry: 16-byte unit k of this lane covers row (lane + 32k) / U
+    const int64_t rowstride = (int64_t)L * K;
+    auto flush = [&](R* __restrict__ out, const R* __restrict__ stage, int tb) {
+      __syncwarp();
+      if (out) {
+#pragma unroll
+        for (int k = 0; k < G::U; ++k) {
+          const int v = lane + kWarp * k;
+          const int row = v / G::U;
+          const int e = (v % G::U) * G::EPU;
+          if (row < C) {
+            R* dst = out + start * K + row * rowstride + (int64_t)tb * K + e;
+            *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(stage + row * G::PITCH + e);
+          }
+        }
+      }
+      __syncwarp();
+    };
+
+    R X[K][K];
+    R st[TR::S][K][LOGHMM_NSLOT];
+    R g0[K], glast[K], pg[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      g0[i] = R(0);
+      glast[i] = R(0);
+      pg[i] = R(0);
+#pragma unroll
+      for (int j = 0; j < K; ++j) X[i][j] = R(0);
+#pragma unroll
+      for (int s = 0; s < TR::S; ++s)
+#pragma unroll
+        for (int q = 0; q < LOGHMM_NSLOT; ++q) st[s][i][q] = R(0);
+    }
+
+    R av[K];  // forward: alpha~_{t-1}
+    R lam = lane == 0 ? R(0) : (R)lam_in;  // t = 0 uses p = pi (linear, offset 0)
+#pragma unroll
+    for (int j = 0; j < K; ++j) av[j] = a_in[j];
+    R bt[K];  // backward: beta~_{t+1}
+    R rho = (R)rho_ex;
+#pragma unroll
+    for (int j = 0; j < K; ++j) bt[j] = b_ex[j];
+    {  // pre-step: beta at the chunk's last step
+      R o[K];
+      const R rl = rho * kLN2;
+#pragma unroll
+      for (int j = 0; j < K; ++j) o[j] = fma(N::flg2(bt[j]), kLN2, rl);
+      SVec<R, K>::st(myB + 3 * K, o);
+      park_st(L - 1, bt);
+    }
+
+    int gcf = rn_groups, gcb = rnb_groups;
+    Y4<R> yf, yf1, yb, yb1;
+    yf.load(y0c);
+    yb.load(y0c + L - 4);
+    if (two) {
+      yf1.load(y1c);
+      yb1.load(y1c + L - 4);
+    }
+
+    // One 4-step group of both directions.  PH2: second half (meet).
+    auto group = [&](int g, auto ph2c) {
+      constexpr bool PH2 = decltype(ph2c)::value;
+      Y4<R> yfn, yfn1, ybn, ybn1;
+      if (g + 1 < NG) {
+        yfn.load(y0c + 4 * (g + 1));
+        ybn.load(y0c + L - 4 * (g + 2));
+        if (two) {
+          yfn1.load(y1c + 4 * (g + 1));
+          ybn1.load(y1c + L - 4 * (g + 2));
+        }
+      }
+#pragma unroll
+      for (int sub = 0; sub < 4; ++sub) {
+        const int i = 4 * g + sub;
+        const int t = L - 2 - i;  // backward step (t = -1: chunk tail, xi pair only)
+        R be[K], al[K];
+        if constexpr (PH2) {
+          // parked vectors: beta~_i for the forward step, alpha~_t for the backward
+          const int ts = t < 0 ? 0 : t;
+          if constexpr (TM) {
+            uint32_t rf[KP], rb[KP];
+            tm_ld(tbase + (uint32_t)(i * KP), rf);
+            tm_ld(tbase + (uint32_t)(ts * KP), rb);
+            tm_wait_ld<KP>(rf, rb);
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              be[j] = (R)__uint_as_float(rf[j]);
+              al[j] = (R)__uint_as_float(rb[j]);
+            }
+          } else {
+            SVec<R, K>::ld(mypark + i * (kWarp * K), be);
+            SVec<R, K>::ld(mypark + ts * (kWarp * K), al);
+          }
+          if (t < 0) {
+#pragma unroll
+            for (int j = 0; j < K; ++j) al[j] = a_in[j];
+          }
+        }
+        // ----------------------- forward step t = i -----------------------
+        {
+          ObsFeat<R> f0, f1;
+          R u[K], bh[K], p[K];
+          const R m = emit(yf.v[sub], two ? yf1.v[sub] : R(0), f0, f1, u, bh);
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            R acc = av[0] * Am[0][c];
+#pragma unroll
+            for (int r = 1; r < K; ++r) acc = fma(av[r], Am[r][c], acc);
+            p[c] = acc;
+          }
+          if (!PH2 && sub == 0) {
+            const bool first = (g == 0) && (lane == 0);
+#pragma unroll
+            for (int j = 0; j < K; ++j) p[j] = first ? pil[j] : p[j];
+          }
+          {
+            R o[K];
+            const R ll2 = lam * kLN2;
+#pragma unroll
+            for (int j = 0; j < K; ++j) o[j] = fma(N::flg2(p[j]) + u[j], kLN2, ll2);
+            SVec<R, K>::st(myA + sub * K, o);
+          }
+          if constexpr (PH2) {
+            R cv[K], gg[K];
+            R Z = R(0);
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              cv[j] = bh[j] * be[j];
+              Z = fma(p[j], cv[j], Z);
+            }
+            const R iz = N::frcp(Z);
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              cv[j] *= iz;
+              gg[j] = p[j] * cv[j];
+            }
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+              for (int c = 0; c < K; ++c) X[r][c] = fma(av[r], cv[c], X[r][c]);
+            SVec<R, K>::st(myGf + sub * K, gg);
+            stats_step<R, K, CFG>(st, gg, em.em, f0, f1);
+            if (sub == 3) {
+#pragma unroll
+              for (int j = 0; j < K; ++j) glast[j] = gg[j];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < K; ++j) av[j] = p[j] * bh[j];
+          lam += m;
+          if (rn_step || (sub == 3 && --gcf == 0)) {
+            if (!rn_step) gcf = rn_groups;
+            renorm_vec<R, K>(av, lam);
+          }
+          if constexpr (!PH2) park_st(i, av);
+        }
+        // ------------- backward step: y index r = t + 1 = L-1-i -------------
+        {
+          ObsFeat<R> f0, f1;
+          R u[K], bh[K], w[K], q[K];
+          const R m = emit(yb.v[3 - sub], two ? yb1.v[3 - sub] : R(0), f0, f1, u, bh);
+#pragma unroll
+          for (int j = 0; j < K; ++j) w[j] = bh[j] * bt[j];
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            R acc = Am[r][0] * w[0];
+#pragma unroll
+            for (int c = 1; c < K; ++c) acc = fma(Am[r][c], w[c], acc);
+            q[r] = acc;
+          }
+          const R rho2 = rho + m;
+          {  // (the t = -1 store lands in an already flushed slot)
+            R o[K];
+            const R rl = rho2 * kLN2;
+#pragma unroll
+            for (int j = 0; j < K; ++j) o[j] = fma(N::flg2(q[j]), kLN2, rl);
+            SVec<R, K>::st(myB + (t & 3) * K, o);
+          }
+          if constexpr (PH2) {
+            // the pending posterior gamma_{t+1} meets the features of y_{t+1}
+            // (the first one is the boundary posterior gamma_{HL-1})
+            stats_step<R, K, CFG>(st, pg, em.em, f0, f1);
+            R Z = R(0);
+#pragma unroll
+            for (int j = 0; j < K; ++j) Z = fma(al[j], q[j], Z);
+            R iz = N::frcp(Z);
+            if (sub == 3) iz = (t < 0 && lane == 0) ? R(0) : iz;  // no pair before t = 0
+            R ai[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) ai[j] = al[j] * iz;
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+              for (int c = 0; c < K; ++c) X[r][c] = fma(ai[r], w[c], X[r][c]);
+#pragma unroll
+            for (int j = 0; j < K; ++j) pg[j] = ai[j] * q[j];
+            SVec<R, K>::st(myGb + (t & 3) * K, pg);
+            if (sub == 2) {  // t = 0 in the last group
+#pragma unroll
+              for (int j = 0; j < K; ++j) g0[j] = pg[j];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < K; ++j) bt[j] = q[j];
+          rho = rho2;
+          if (rnb_step || (sub == 3 && --gcb == 0)) {
+            if (!rnb_step) gcb = rnb_groups;
+            renorm_vec<R, K>(bt, rho);
+          }
+          if constexpr (!PH2) {
+            if (t >= HL) park_st(t, bt);
+          }
+        }
+        if (sub == 2) {  // backward slabs [L-4-4g, L-4g) complete
+          const int tb = L - 4 - 4 * g;
+          flush(outB, stB, tb);
+          if constexpr (PH2) flush(outG, stGb, tb);
+        }
+      }
+      flush(outA, stA, 4 * g);  // forward slabs [4g, 4g+4) complete
+      if constexpr (PH2) flush(outG, stGf, 4 * g);
+      yf = yfn;
+      yb = ybn;
+      if (two) {
+        yf1 = yfn1;
+        yb1 = ybn1;
+      }
+    };
+
+#pragma unroll 1
+    for (int g = 0; g < NG / 2; ++g) group(g, std::false_type{});
+    {
+      // boundary: gamma_{HL-1} from alpha~_{HL-1} (av) and beta~_{HL-1} (bt);
+      // it is the first pending posterior of the backward direction
+      if constexpr (TM) tm_wait_st();
+      R Z = R(0);
+#pragma unroll
+      for (int j = 0; j < K; ++j) Z = fma(av[j], bt[j], Z);
+      const R iz = N::frcp(Z);
+#pragma unroll
+      for (int j = 0; j < K; ++j) pg[j] = av[j] * bt[j] * iz;
+      SVec<R, K>::st(myGb + 3 * K, pg);
+      __syncwarp();
+    }
+#pragma unroll 1
+    for (int g = NG / 2; g < NG; ++g) group(g, std::true_type{});
+
+    // ===================== per-sequence results =============================
+    if (!act) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) X[i][j] = R(0);
+#pragma unroll
+        for (int s = 0; s < TR::S; ++s)
+#pragma unroll
+          for (int q = 0; q < LOGHMM_NSLOT; ++q) st[s][i][q] = R(0);
+      }
+    }
+    // rare path: exact first dead step and NaN flag (rescan of the chunk)
+    int dead_t = INT_MAX;
+    bool nan_seen = false;
+    if (__any_sync(kFull, bad)) {
+      if (bad) {
+        for (int s = 0; s < L; ++s) {
+          const R yv0 = y0c[s];
+          const R yv1 = two ? y1c[s] : R(0);
+          if (yv0 != yv0 || yv1 != yv1) nan_seen = true;
+          ObsFeat<R> f0, f1;
+          R u[K];
+          em.eval(yv0, yv1, f0, f1, u, oob);
+          R m = u[0];
+#pragma unroll
+          for (int j = 1; j < K; ++j) m = fmax(m, u[j]);
+          if (!(m > N::ninf()) && dead_t == INT_MAX) dead_t = t0 + s;
+        }
+      }
+    }
+    const int dead_all = (int)warp_min_ll((long long)dead_t);
+    const unsigned nanb = __ballot_sync(kFull, nan_seen);
+    const unsigned oobb = __ballot_sync(kFull, oob && act);
+    if (lane == 0) {
+      a.ll[b] = dead_all == INT_MAX ? LL : -CUDART_INF;
+      if (a.flags) {
+        a.flags[2 * b] = dead_all == INT_MAX ? -1 : (int64_t)dead_all;
+        a.flags[2 * b + 1] = (nanb ? 1 : 0) | (oobb ? 2 : 0);
+      }
+    }
+    if (a.partials) {
+      double* row = a.partials + b * a.stats_width;
+      int idx = 0;
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const R v = warp_sum(X[i][j]);
+          if (lane == (idx & 31)) row[idx] = (double)v * (double)Am[i][j];
+          ++idx;
+        }
+      // gamma totals over t < T-1 = all-step mass minus the last posterior
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const R v = warp_sum(st[0][j][0] - (lane == C - 1 ? glast[j] : R(0)));
+        if (lane == (idx & 31)) row[idx] = (double)v;
+        ++idx;
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const R v = __shfl_sync(kFull, g0[j], 0);
+        if (lane == (idx & 31)) row[idx] = (double)v;
+        ++idx;
+      }
+#pragma unroll
+      for (int s = 0; s < TR::S; ++s)
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+#pragma unroll
+          for (int q = 0; q < LOGHMM_NSLOT; ++q) {
+            const int ns = s == 0 ? TR::NS0 : TR::NS1;
+            R v = R(0);
+            if (q < ns) v = warp_sum(st[s][j][q]);
+            if (lane == (idx & 31)) row[idx] = (double)v;
+            ++idx;
+          }
+      for (; idx < a.stats_width; ++idx)
+        if (lane == (idx & 31)) row[idx] = 0.0;
+    }
+  }
+
+  if constexpr (TM) {
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    if (wib == 0) {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem),
+                   "r"((uint32_t)a.tm_cols)
+                   : "memory");
+    }
+  }
+}
+
+}  // namespace lhmm

@@ -3,7 +3,7 @@
 #pragma once
 
 // Translation units that instantiate one kernel family define LHMM_ONLY_FB,
-// LHMM_ONLY_VIT or LHMM_ONLY_FBM first, so they depend on (and parse) only
+// LHMM_ONLY_VIT or LHMM_ONLY_FBC first, so they depend on (and parse) only
 // that family's header; hmm_capi.cu sees every declaration.
 #if defined(LHMM_ONLY_FB)
 #include "hmm_fb.cuh"
@@ -11,17 +11,17 @@
 #elif defined(LHMM_ONLY_VIT)
 #include "hmm_viterbi2.cuh"
 #define LHMM_HAS_VIT 1
-#elif defined(LHMM_ONLY_FBM)
-#include "hmm_fbm.cuh"
-#define LHMM_HAS_FBM 1
+#elif defined(LHMM_ONLY_FBC)
+#include "hmm_fbc.cuh"
+#define LHMM_HAS_FBC 1
 #else
 #include "hmm_fb.cuh"
-#include "hmm_fbm.cuh"
+#include "hmm_fbc.cuh"
 #include "hmm_viterbi.cuh"
 #include "hmm_viterbi2.cuh"
 #define LHMM_HAS_FB 1
 #define LHMM_HAS_VIT 1
-#define LHMM_HAS_FBM 1
+#define LHMM_HAS_FBC 1
 #endif
 
 namespace lhmm {
@@ -120,32 +120,39 @@ cudaError_t launch_vit2(const VitArgs& a, int cfg, dim3 grid, dim3 block, size_t
 }
 #endif  // LHMM_HAS_VIT
 
-#if defined(LHMM_HAS_FBM)
+#if defined(LHMM_HAS_FBC)
 template <typename R, int K, int CFG>
-static cudaError_t launch_fbm_one(const FBMArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-  auto fn = fb_mitm_kernel<R, K, CFG>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  fn<<<grid, 64, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename R, int K>
-cudaError_t launch_fb_mitm(const FBMArgs& a, int cfg, dim3 grid, size_t smem, cudaStream_t st) {
-  switch (cfg) {
-    case kCfgGauss: return launch_fbm_one<R, K, kCfgGauss>(a, grid, smem, st);
-    case kCfgStudent: return launch_fbm_one<R, K, kCfgStudent>(a, grid, smem, st);
-    case kCfgGamma: return launch_fbm_one<R, K, kCfgGamma>(a, grid, smem, st);
-    case kCfgVonMises: return launch_fbm_one<R, K, kCfgVonMises>(a, grid, smem, st);
-    case kCfgPoisson: return launch_fbm_one<R, K, kCfgPoisson>(a, grid, smem, st);
-    case kCfgGammaVM: return launch_fbm_one<R, K, kCfgGammaVM>(a, grid, smem, st);
-    default: return launch_fbm_one<R, K, kCfgMixed>(a, grid, smem, st);
+static cudaError_t launch_fbc_one(const FBCArgs& a, dim3 grid, dim3 block, size_t smem,
+                                  cudaStream_t st) {
+  if constexpr (K >= 2) {
+    auto fn = fb_chunk_kernel<R, K, CFG>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, block, smem, st>>>(a);
+    return cudaGetLastError();
+  } else {
+    return cudaErrorInvalidValue;
   }
 }
 
 template <typename R, int K>
-size_t fb_mitm_smem() { return MISmem<R, K>::bytes(); }
-#endif  // LHMM_HAS_FBM
+cudaError_t launch_fb_chunk(const FBCArgs& a, int cfg, dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st) {
+  switch (cfg) {
+    case kCfgGauss: return launch_fbc_one<R, K, kCfgGauss>(a, grid, block, smem, st);
+    case kCfgStudent: return launch_fbc_one<R, K, kCfgStudent>(a, grid, block, smem, st);
+    case kCfgGamma: return launch_fbc_one<R, K, kCfgGamma>(a, grid, block, smem, st);
+    case kCfgVonMises: return launch_fbc_one<R, K, kCfgVonMises>(a, grid, block, smem, st);
+    case kCfgPoisson: return launch_fbc_one<R, K, kCfgPoisson>(a, grid, block, smem, st);
+    case kCfgGammaVM: return launch_fbc_one<R, K, kCfgGammaVM>(a, grid, block, smem, st);
+    default: return launch_fbc_one<R, K, kCfgMixed>(a, grid, block, smem, st);
+  }
+}
+
+// shared-memory elements of one warp for chunk length L
+template <typename R, int K>
+int fb_chunk_warp_elems(int L) { return FBCGeom<R, K>::warp_elems(L); }
+#endif  // LHMM_HAS_FBC
 
 #define LHMM_INST_FB(R, K)                                                                   \
   template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \
@@ -154,9 +161,9 @@ size_t fb_mitm_smem() { return MISmem<R, K>::bytes(); }
   template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
                                               cudaStream_t);                                 \
   template cudaError_t launch_vit2<R, K>(const VitArgs&, int, dim3, dim3, size_t, cudaStream_t);
-#define LHMM_INST_FBM(R, K)                                                                  \
-  template cudaError_t launch_fb_mitm<R, K>(const FBMArgs&, int, dim3, size_t, cudaStream_t); \
-  template size_t fb_mitm_smem<R, K>();
+#define LHMM_INST_FBC(R, K)                                                                  \
+  template cudaError_t launch_fb_chunk<R, K>(const FBCArgs&, int, dim3, dim3, size_t, cudaStream_t); \
+  template int fb_chunk_warp_elems<R, K>(int);
 
 #define LHMM_EXTERN_INST(R, K)                                                                      \
   extern template cudaError_t launch_fb_small<R, K>(const FBArgs&, int, bool, dim3, dim3, size_t,   \
@@ -164,7 +171,7 @@ size_t fb_mitm_smem() { return MISmem<R, K>::bytes(); }
   extern template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
                                                      cudaStream_t);                                 \
   extern template cudaError_t launch_vit2<R, K>(const VitArgs&, int, dim3, dim3, size_t, cudaStream_t); \
-  extern template cudaError_t launch_fb_mitm<R, K>(const FBMArgs&, int, dim3, size_t, cudaStream_t); \
-  extern template size_t fb_mitm_smem<R, K>();
+  extern template cudaError_t launch_fb_chunk<R, K>(const FBCArgs&, int, dim3, dim3, size_t, cudaStream_t); \
+  extern template int fb_chunk_warp_elems<R, K>(int);
 
 }  // namespace lhmm

@@ -1,0 +1,6 @@
+// Explicit instantiation: chunked meet-in-the-middle FB kernels for dtype double, K=3.
+#define LHMM_ONLY_FBC
+#include "hmm_launch.cuh"
+namespace lhmm {
+LHMM_INST_FBC(double, 3)
+}

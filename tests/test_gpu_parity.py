@@ -183,11 +183,86 @@ def test_fp64_viterbi_poisson_bitexact(K, vit_algo):
         assert out.log_joint.cpu().numpy()[b] == j
 
 
-@pytest.fixture(params=["chunked", "mitm"])
+@pytest.fixture(params=["chunked", "auto"])
 def fb_algo(request, monkeypatch):
-    """Run a test under both forward-backward decompositions."""
-    monkeypatch.setenv("LOGHMM_FB_ALGO", request.param)
+    """Run a test under both forward-backward decompositions: the chunked scan
+    (forced) and the automatic choice, which takes the chunk-operator +
+    meet-in-the-middle kernel for equal-length batches."""
+    if request.param == "chunked":
+        monkeypatch.setenv("LOGHMM_FB_ALGO", "chunked")
+    else:
+        monkeypatch.delenv("LOGHMM_FB_ALGO", raising=False)
     return request.param
+
+
+@pytest.mark.parametrize("K", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("T", [8, 64, 1000, 1024])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_posteriors_equal_length(K, T, dtype, fb_algo):
+    """Equal-length batches (the [B, T] layout of the BASELINE configs) under
+    both decompositions against the oracle: LL, gamma, log alpha, log beta."""
+    rng = np.random.default_rng(100 * K + T)
+    m = _random_gauss_model(rng, K)
+    seqs = [rng.normal(0, 3, T) for _ in range(5)]
+    r = H.posteriors_batch(m, seqs, dtype=dtype)
+    lp, la = O.model_tables(m.initial, m.transitions)
+    g = r.gamma.cpu().numpy().astype(np.float64)
+    A_ = r.log_alpha.cpu().numpy().astype(np.float64)
+    B_ = r.log_beta.cpu().numpy().astype(np.float64)
+    ll = r.log_likelihood.cpu().numpy()
+    for b, y in enumerate(seqs):
+        yy = y.astype(np.float32).astype(np.float64) if dtype == "float32" else y
+        o = O.posteriors(lp, la, O.emission_matrix(to_tuples(m), yy))
+        s = slice(b * T, (b + 1) * T)
+        if dtype == "float64":
+            assert ll[b] == pytest.approx(o["ll"], rel=1e-9)
+            np.testing.assert_allclose(g[s], o["gamma"], atol=1e-9)
+            np.testing.assert_allclose(A_[s], o["log_alpha"], rtol=1e-9, atol=1e-9)
+            np.testing.assert_allclose(B_[s], o["log_beta"], rtol=1e-9, atol=1e-9)
+        else:
+            assert ll[b] == pytest.approx(o["ll"], rel=1e-4)
+            np.testing.assert_allclose(g[s], o["gamma"], atol=1e-5)
+            np.testing.assert_allclose(A_[s], o["log_alpha"], rtol=1e-5, atol=1e-3)
+            np.testing.assert_allclose(B_[s], o["log_beta"], rtol=1e-5, atol=1e-3)
+
+
+def _estep_partials(model, data, dtype, algo, monkeypatch):
+    if algo == "chunked":
+        monkeypatch.setenv("LOGHMM_FB_ALGO", "chunked")
+    else:
+        monkeypatch.delenv("LOGHMM_FB_ALGO", raising=False)
+    dm = engine.DeviceModel.from_model(model)
+    batch = engine.make_batch(data, model.n_streams, dtype)
+    o = engine.forward_backward(batch, dm, stats=True)
+    return o.partials.cpu().numpy(), o.ll.cpu().numpy(), o.flags.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,B,T", [("c2", 6, 1024), ("c3", 4, 2048), ("c4", 4, 2000),
+                                      ("pois4", 4, 512)])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_estep_statistics_both_decompositions(name, B, T, dtype, monkeypatch):
+    """Per-sequence E-step statistics (xi totals, gamma totals, gamma_0, family
+    sums) of the meet-in-the-middle kernel equal the chunked scan's, for every
+    family configuration it serves (Gaussian, Student-t, Gamma+von Mises,
+    Poisson)."""
+    if name == "pois4":
+        rng = np.random.default_rng(3)
+        K = 4
+        A = rng.dirichlet(np.ones(K), size=K) * 0.3 + 0.7 * np.eye(K)
+        A /= A.sum(1, keepdims=True)
+        model = H.HmmModel(np.full(K, 1 / K), A, tuple(H.Poisson(0.5 * (k + 1)) for k in range(K)))
+        data = [rng.poisson(2.0, T).astype(np.float64) for _ in range(B)]
+    else:
+        cfg = make_config(name, B=B, T=T)
+        model = cfg.init
+        data = [cfg.data[b] for b in range(B)]
+    pa, la, fa = _estep_partials(model, data, dtype, "auto", monkeypatch)
+    pc, lc, fc = _estep_partials(model, data, dtype, "chunked", monkeypatch)
+    rt = 1e-9 if dtype == "float64" else 2e-4
+    np.testing.assert_allclose(la, lc, rtol=rt)
+    np.testing.assert_array_equal(fa, fc)
+    scale = np.abs(pc).max(axis=1, keepdims=True) + 1e-300
+    np.testing.assert_allclose(pa / scale, pc / scale, atol=rt * 10)
 
 
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 6, 8])
