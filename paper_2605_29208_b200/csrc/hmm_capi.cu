@@ -501,7 +501,8 @@ int32_t loghmm_reduce_mstep(const double* partials, const double* ll, int64_t B,
   double* part = (double*)workspace;
   unsigned* counter =
       (unsigned*)((char*)workspace + align256((size_t)kReduceBlocks * (size_t)(width + 1) * 8));
-  const size_t smem = (size_t)(width + 1) * sizeof(double);
+  // totals + one row of column sums per thread group (see the kernel)
+  const size_t smem = (size_t)(width + 1 + 256) * sizeof(double);
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(reduce_mstep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)

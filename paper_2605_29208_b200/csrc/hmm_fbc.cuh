@@ -128,6 +128,155 @@ struct Y4 {
   }
 };
 
+// ---------------------------------------------------------------------------
+// K-vector arithmetic.  For fp32 and even K the pairs (x[2k], x[2k+1]) go
+// through Blackwell's packed FFMA2 / FMUL2 / FADD2 (one issue slot for two
+// lanes of math; a scalar operand is broadcast by the instruction itself), so
+// the matrix-vector steps of the recursions cost half the issue slots.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void f2_fma(float& d0, float& d1, float a0, float a1, float b0, float b1,
+                                       float c0, float c1) {
+  asm("{.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void f2_mul(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void f2_add(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void f2_sub(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "sub.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+template <typename R, int K>
+struct V {
+  static constexpr bool P = sizeof(R) == 4 && (K % 2) == 0;
+  typedef R A[K];
+  // d = s * x
+  static __device__ __forceinline__ void mul_s(A& d, R s, const A& x) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_mul(d[k], d[k + 1], s, s, x[k], x[k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = s * x[k];
+    }
+  }
+  // d = s * x + c
+  static __device__ __forceinline__ void fma_s(A& d, R s, const A& x, const A& c) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_fma(d[k], d[k + 1], s, s, x[k], x[k + 1], c[k], c[k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = ::fma(s, x[k], c[k]);
+    }
+  }
+  // d = x * y
+  static __device__ __forceinline__ void mul(A& d, const A& x, const A& y) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_mul(d[k], d[k + 1], x[k], x[k + 1], y[k], y[k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = x[k] * y[k];
+    }
+  }
+  // d = x * y + c
+  static __device__ __forceinline__ void fma(A& d, const A& x, const A& y, const A& c) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_fma(d[k], d[k + 1], x[k], x[k + 1], y[k], y[k + 1], c[k], c[k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = ::fma(x[k], y[k], c[k]);
+    }
+  }
+  // d = x + y
+  static __device__ __forceinline__ void add(A& d, const A& x, const A& y) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_add(d[k], d[k + 1], x[k], x[k + 1], y[k], y[k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = x[k] + y[k];
+    }
+  }
+  // d = x - s
+  static __device__ __forceinline__ void sub_s(A& d, const A& x, R s) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_sub(d[k], d[k + 1], x[k], x[k + 1], s, s);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = x[k] - s;
+    }
+  }
+  // d = x - y
+  static __device__ __forceinline__ void sub(A& d, const A& x, const A& y) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_sub(d[k], d[k + 1], x[k], x[k + 1], y[k], y[k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = x[k] - y[k];
+    }
+  }
+  // d = s - x
+  static __device__ __forceinline__ void rsub_s(A& d, R s, const A& x) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_sub(d[k], d[k + 1], s, s, x[k], x[k + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = s - x[k];
+    }
+  }
+  // d = s * x + c (scalar s, c)
+  static __device__ __forceinline__ void fma_ss(A& d, R s, const A& x, R c) {
+    if constexpr (P) {
+#pragma unroll
+      for (int k = 0; k < K; k += 2) f2_fma(d[k], d[k + 1], s, s, x[k], x[k + 1], c, c);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) d[k] = ::fma(s, x[k], c);
+    }
+  }
+  // sum_k x[k] * y[k]
+  static __device__ __forceinline__ R dot(const A& x, const A& y) {
+    if constexpr (P) {
+      R a0, a1;
+      f2_mul(a0, a1, x[0], x[1], y[0], y[1]);
+#pragma unroll
+      for (int k = 2; k < K; k += 2) f2_fma(a0, a1, x[k], x[k + 1], y[k], y[k + 1], a0, a1);
+      return a0 + a1;
+    } else {
+      R a = x[0] * y[0];
+#pragma unroll
+      for (int k = 1; k < K; ++k) a = ::fma(x[k], y[k], a);
+      return a;
+    }
+  }
+  static __device__ __forceinline__ R vmax(const A& x) {
+    R m = x[0];
+#pragma unroll
+    for (int k = 1; k < K; ++k) m = fmax(m, x[k]);
+    return m;
+  }
+};
+
 // Emission log2-densities of all states (u_j = log2 b_j(y)).  The Gaussian is
 // rewritten as u = c - w^2 with w = y*s - mu*s, s = sqrt(log2(e)/2)/sigma.
 template <typename R, int K, int CFG>
@@ -152,11 +301,10 @@ struct Em2 {
                                        bool& oob) const {
     if constexpr (CFG == kCfgGauss) {
       f0.y = y0;
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const R w = fma(y0, ga[j], go[j]);
-        u[j] = fma(-w, w, gc[j]);
-      }
+      R w[K], w2[K];
+      V<R, K>::fma_s(w, y0, ga, go);
+      V<R, K>::mul(w2, w, w);
+      V<R, K>::sub(u, gc, w2);
     } else {
       R lb[K];
       em.eval(y0, y1, f0, f1, lb, oob);
@@ -255,6 +403,26 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 
 constexpr int kFbcWarps = 4;  // warps (sequences) per CTA: one warpgroup
 
+// Power-of-two normalisation of a scan operator (FMNMX max; exponent kept in
+// a double log2 offset).
+template <typename R, int K>
+__device__ __forceinline__ void norm_op(R (&Z)[K][K], double& off2) {
+  R m = Z[0][0];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int c = 0; c < K; ++c) m = fmax(m, Z[r][c]);
+  if (m > R(0)) {
+    int e;
+    const R s = Num<R>::pow2_scale(m, e);
+    off2 += (double)e;
+#pragma unroll
+    for (int r = 0; r < K; ++r) V<R, K>::mul_s(Z[r], s, Z[r]);
+  } else {
+    off2 = -CUDART_INF;
+  }
+}
+
 template <typename R, int K, int CFG>
 __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
   typedef Num<R> N;
@@ -337,34 +505,34 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
     }
     Em2<R, K, CFG> em;
     em.load(md, a.n_streams, a.stream_fams, a.lut, a.lut_n);
-    // Renormalise every nn steps: the max entry of the operator / forward
-    // vector shrinks by at most min(A) per step (the backward vector by at
-    // most min(A)^2), so nn steps stay above 2^-100 (fp32) / 2^-900 (fp64).
-    int nn = 1, nnb = 1;
+    // Pass-1 operator renormalisation every nn steps: its max entry shrinks
+    // by at most min(A) per step, so nn steps stay above 2^-100 (fp32) /
+    // 2^-900 (fp64).  (Pass 2 renormalises every step through the emission
+    // shift instead.)
+    int nn = 1;
     if (minA > R(0)) {
       const double lg = -log2((double)minA);
       const double budget = sizeof(R) == 4 ? 100.0 : 900.0;
       nn = lg <= 0.0 ? 8 : (int)fmin(8.0, fmax(1.0, floor(budget / lg)));
-      nnb = lg <= 0.0 ? 8 : (int)fmin(8.0, fmax(1.0, floor(budget / (2.0 * lg))));
     }
-    // every step (nn < 4) or every 1 / 2 four-step groups
-    const bool rn_step = nn < 4, rnb_step = nnb < 4;
-    const int rn_groups = nn >= 8 ? 2 : 1, rnb_groups = nnb >= 8 ? 2 : 1;
+    // pass-1 operator: every step (nn < 4) or every 1 / 2 four-step groups
+    const bool rn_step = nn < 4;
+    const int rn_groups = nn >= 8 ? 2 : 1;
 
     const R* __restrict__ y0c = reinterpret_cast<const R*>(a.y0) + start + t0;
     const R* __restrict__ y1c = two ? reinterpret_cast<const R*>(a.y1) + start + t0 : y0c;
 
     bool oob = false, bad = false;
 
-    // u_j = log2 b_j(y), m = max_j u_j clamped finite, bh_j = 2^(u_j - m)
-    auto emit = [&](R yv0, R yv1, ObsFeat<R>& f0, ObsFeat<R>& f1, R (&u)[K], R (&bh)[K]) -> R {
+    // u_j = log2 b_j(y), m = max_j u_j clamped finite; returns m' = m + shift
+    // and bh_j = 2^(u_j - m') (the shift renormalises the carried vector)
+    auto emit = [&](R yv0, R yv1, ObsFeat<R>& f0, ObsFeat<R>& f1, R (&u)[K], R (&bh)[K],
+                    R shift) -> R {
       em.eval(yv0, yv1, f0, f1, u, oob);
-      R m = u[0];
+      const R m = fmax(V<R, K>::vmax(u), kFloor) + shift;
+      V<R, K>::sub_s(bh, u, m);
 #pragma unroll
-      for (int j = 1; j < K; ++j) m = fmax(m, u[j]);
-      m = fmax(m, kFloor);
-#pragma unroll
-      for (int j = 0; j < K; ++j) bh[j] = N::fex2(u[j] - m);
+      for (int j = 0; j < K; ++j) bh[j] = N::fex2(bh[j]);
       return m;
     };
 
@@ -395,18 +563,17 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
           const R yv1 = two ? yc1.v[sub] : R(0);
           ObsFeat<R> f0, f1;
           R u[K], bh[K];
-          const R m = emit(yv0, yv1, f0, f1, u, bh);
+          const R m = emit(yv0, yv1, f0, f1, u, bh, R(0));
           bad |= !(m > kFloor);  // a dead step (all -inf) or NaN observation
-          R Nw[K][K];
+          R Ab[K][K], Nw[K][K];  // A diag(bh), then Mop A diag(bh)
 #pragma unroll
-          for (int r = 0; r < K; ++r)
+          for (int i = 0; i < K; ++i) V<R, K>::mul(Ab[i], Am[i], bh);
 #pragma unroll
-            for (int c = 0; c < K; ++c) {
-              R acc = Mop[r][0] * Am[0][c];
+          for (int r = 0; r < K; ++r) {
+            V<R, K>::mul_s(Nw[r], Mop[r][0], Ab[0]);
 #pragma unroll
-              for (int i = 1; i < K; ++i) acc = fma(Mop[r][i], Am[i][c], acc);
-              Nw[r][c] = acc * bh[c];
-            }
+            for (int i = 1; i < K; ++i) V<R, K>::fma_s(Nw[r], Mop[r][i], Ab[i], Nw[r]);
+          }
           if (sub == 0) {
             // t = 0 (lane 0, first group) seeds the forward vector
             // (log2 pi + log2 b_0): no operator step
@@ -437,9 +604,7 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
               const R s = N::pow2_scale(mx, e);
               moff += (R)e;
 #pragma unroll
-              for (int r = 0; r < K; ++r)
-#pragma unroll
-                for (int c = 0; c < K; ++c) Mop[r][c] *= s;
+              for (int r = 0; r < K; ++r) V<R, K>::mul_s(Mop[r], s, Mop[r]);
             }
           }
         }
@@ -488,7 +653,7 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
 #pragma unroll
             for (int c = 0; c < K; ++c) Q[r][c] = Z[r][c];
           qo += po;
-          normalise_mat2<R, K>(Q, qo);
+          norm_op<R, K>(Q, qo);
         }
       }
       R sm = seed_u[0];
@@ -544,7 +709,7 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
 #pragma unroll
             for (int c = 0; c < K; ++c) S[r][c] = Z[r][c];
           so += yo;
-          normalise_mat2<R, K>(S, so);
+          norm_op<R, K>(S, so);
         }
       }
       R z[K];
@@ -570,33 +735,49 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
     R* __restrict__ outA = reinterpret_cast<R*>(a.log_alpha);
     R* __restrict__ outB = reinterpret_cast<R*>(a.log_beta);
     R* __restrict__ outG = reinterpret_cast<R*>(a.gamma);
-    // flush geometry: 16-byte unit k of this lane covers row (lane + 32k) / U
+    // Flush geometry: 16-byte unit k of this lane is unit (lane + 32k) % U of
+    // slab row (lane + 32k) / U.  When U divides 32 the row advances by 32/U
+    // per k and the unit is fixed, so one element offset per lane suffices.
+    constexpr bool kUdiv = (kWarp % G::U) == 0;
     const int64_t rowstride = (int64_t)L * K;
+    const int f_row0 = kUdiv ? lane / G::U : 0;
+    const int f_e = kUdiv ? (lane % G::U) * G::EPU : 0;
+    const int64_t f_off0 = (int64_t)f_row0 * rowstride + f_e;  // element offset inside the sequence
     auto flush = [&](R* __restrict__ out, const R* __restrict__ stage, int tb) {
       __syncwarp();
-      if (out) {
+      R* __restrict__ ob = out + start * K + (int64_t)tb * K;
 #pragma unroll
-        for (int k = 0; k < G::U; ++k) {
+      for (int k = 0; k < G::U; ++k) {
+        int row, e;
+        int64_t off;
+        if constexpr (kUdiv) {
+          row = f_row0 + k * (kWarp / G::U);
+          e = f_e;
+          off = f_off0 + (int64_t)k * (kWarp / G::U) * rowstride;
+        } else {
           const int v = lane + kWarp * k;
-          const int row = v / G::U;
-          const int e = (v % G::U) * G::EPU;
-          if (row < C) {
-            R* dst = out + start * K + row * rowstride + (int64_t)tb * K + e;
-            *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(stage + row * G::PITCH + e);
-          }
+          row = v / G::U;
+          e = (v % G::U) * G::EPU;
+          off = row * rowstride + e;
         }
+        if (row < C)
+          *reinterpret_cast<float4*>(ob + off) = *reinterpret_cast<const float4*>(stage + row * G::PITCH + e);
       }
       __syncwarp();
     };
 
     R X[K][K];
     R st[TR::S][K][LOGHMM_NSLOT];
+    R gs0[K], gs1[K], gs2[K];  // Gaussian statistics (w, w d, w d^2), packed
+    R mu[K];                   // Gaussian means (statistics shift)
     R g0[K], glast[K], pg[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       g0[i] = R(0);
       glast[i] = R(0);
       pg[i] = R(0);
+      gs0[i] = gs1[i] = gs2[i] = R(0);
+      mu[i] = em.em.e0[i].q[0];
 #pragma unroll
       for (int j = 0; j < K; ++j) X[i][j] = R(0);
 #pragma unroll
@@ -604,6 +785,19 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
 #pragma unroll
         for (int q = 0; q < LOGHMM_NSLOT; ++q) st[s][i][q] = R(0);
     }
+    // E-step statistics of one posterior vector g at observation features f
+    auto stats = [&](const R (&g)[K], const ObsFeat<R>& f0, const ObsFeat<R>& f1) {
+      if constexpr (CFG == kCfgGauss) {
+        R d[K], wd[K];
+        V<R, K>::rsub_s(d, f0.y, mu);
+        V<R, K>::mul(wd, g, d);
+        V<R, K>::add(gs0, gs0, g);
+        V<R, K>::add(gs1, gs1, wd);
+        V<R, K>::fma(gs2, wd, d, gs2);
+      } else {
+        stats_step<R, K, CFG>(st, g, em.em, f0, f1);
+      }
+    };
 
     R av[K];  // forward: alpha~_{t-1}
     R lam = lane == 0 ? R(0) : (R)lam_in;  // t = 0 uses p = pi (linear, offset 0)
@@ -614,15 +808,14 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
 #pragma unroll
     for (int j = 0; j < K; ++j) bt[j] = b_ex[j];
     {  // pre-step: beta at the chunk's last step
-      R o[K];
-      const R rl = rho * kLN2;
+      R o[K], l2[K];
 #pragma unroll
-      for (int j = 0; j < K; ++j) o[j] = fma(N::flg2(bt[j]), kLN2, rl);
+      for (int j = 0; j < K; ++j) l2[j] = N::flg2(bt[j]);
+      V<R, K>::fma_ss(o, kLN2, l2, rho * kLN2);
       SVec<R, K>::st(myB + 3 * K, o);
       park_st(L - 1, bt);
     }
 
-    int gcf = rn_groups, gcb = rnb_groups;
     Y4<R> yf, yf1, yb, yb1;
     yf.load(y0c);
     yb.load(y0c + L - 4);
@@ -631,7 +824,9 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
       yb1.load(y1c + L - 4);
     }
 
-    // One 4-step group of both directions.  PH2: second half (meet).
+    // One 4-step group of both directions.  PH2: second half (meet).  The
+    // carried vectors are renormalised every step through the emission shift:
+    // scaling by 2^-log2(max v) keeps max v in [min(A)^2 / 2, 2].
     auto group = [&](int g, auto ph2c) {
       constexpr bool PH2 = decltype(ph2c)::value;
       Y4<R> yfn, yfn1, ybn, ybn1;
@@ -665,109 +860,81 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
             SVec<R, K>::ld(mypark + i * (kWarp * K), be);
             SVec<R, K>::ld(mypark + ts * (kWarp * K), al);
           }
-          if (t < 0) {
+          if (sub == 3) {
+            const bool tail = t < 0;
 #pragma unroll
-            for (int j = 0; j < K; ++j) al[j] = a_in[j];
+            for (int j = 0; j < K; ++j) al[j] = tail ? a_in[j] : al[j];
           }
         }
         // ----------------------- forward step t = i -----------------------
         {
+          const R sf = fmax(N::flg2(V<R, K>::vmax(av)), kFloor);
           ObsFeat<R> f0, f1;
           R u[K], bh[K], p[K];
-          const R m = emit(yf.v[sub], two ? yf1.v[sub] : R(0), f0, f1, u, bh);
+          const R m = emit(yf.v[sub], two ? yf1.v[sub] : R(0), f0, f1, u, bh, sf);
+          V<R, K>::mul_s(p, av[0], Am[0]);
 #pragma unroll
-          for (int c = 0; c < K; ++c) {
-            R acc = av[0] * Am[0][c];
-#pragma unroll
-            for (int r = 1; r < K; ++r) acc = fma(av[r], Am[r][c], acc);
-            p[c] = acc;
-          }
+          for (int r = 1; r < K; ++r) V<R, K>::fma_s(p, av[r], Am[r], p);
           if (!PH2 && sub == 0) {
             const bool first = (g == 0) && (lane == 0);
 #pragma unroll
             for (int j = 0; j < K; ++j) p[j] = first ? pil[j] : p[j];
           }
           {
-            R o[K];
-            const R ll2 = lam * kLN2;
+            R o[K], l2[K];
 #pragma unroll
-            for (int j = 0; j < K; ++j) o[j] = fma(N::flg2(p[j]) + u[j], kLN2, ll2);
+            for (int j = 0; j < K; ++j) l2[j] = N::flg2(p[j]);
+            V<R, K>::add(l2, l2, u);
+            V<R, K>::fma_ss(o, kLN2, l2, lam * kLN2);
             SVec<R, K>::st(myA + sub * K, o);
           }
           if constexpr (PH2) {
             R cv[K], gg[K];
-            R Z = R(0);
+            V<R, K>::mul(cv, bh, be);
+            const R iz = N::frcp(V<R, K>::dot(p, cv));
+            V<R, K>::mul_s(cv, iz, cv);
+            V<R, K>::mul(gg, p, cv);
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-              cv[j] = bh[j] * be[j];
-              Z = fma(p[j], cv[j], Z);
-            }
-            const R iz = N::frcp(Z);
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-              cv[j] *= iz;
-              gg[j] = p[j] * cv[j];
-            }
-#pragma unroll
-            for (int r = 0; r < K; ++r)
-#pragma unroll
-              for (int c = 0; c < K; ++c) X[r][c] = fma(av[r], cv[c], X[r][c]);
+            for (int r = 0; r < K; ++r) V<R, K>::fma_s(X[r], av[r], cv, X[r]);
             SVec<R, K>::st(myGf + sub * K, gg);
-            stats_step<R, K, CFG>(st, gg, em.em, f0, f1);
+            stats(gg, f0, f1);
             if (sub == 3) {
 #pragma unroll
               for (int j = 0; j < K; ++j) glast[j] = gg[j];
             }
           }
-#pragma unroll
-          for (int j = 0; j < K; ++j) av[j] = p[j] * bh[j];
+          V<R, K>::mul(av, p, bh);
           lam += m;
-          if (rn_step || (sub == 3 && --gcf == 0)) {
-            if (!rn_step) gcf = rn_groups;
-            renorm_vec<R, K>(av, lam);
-          }
           if constexpr (!PH2) park_st(i, av);
         }
         // ------------- backward step: y index r = t + 1 = L-1-i -------------
         {
+          const R sb = fmax(N::flg2(V<R, K>::vmax(bt)), kFloor);
           ObsFeat<R> f0, f1;
           R u[K], bh[K], w[K], q[K];
-          const R m = emit(yb.v[3 - sub], two ? yb1.v[3 - sub] : R(0), f0, f1, u, bh);
+          const R m = emit(yb.v[3 - sub], two ? yb1.v[3 - sub] : R(0), f0, f1, u, bh, sb);
+          V<R, K>::mul(w, bh, bt);
 #pragma unroll
-          for (int j = 0; j < K; ++j) w[j] = bh[j] * bt[j];
-#pragma unroll
-          for (int r = 0; r < K; ++r) {
-            R acc = Am[r][0] * w[0];
-#pragma unroll
-            for (int c = 1; c < K; ++c) acc = fma(Am[r][c], w[c], acc);
-            q[r] = acc;
-          }
+          for (int r = 0; r < K; ++r) q[r] = V<R, K>::dot(Am[r], w);
           const R rho2 = rho + m;
           {  // (the t = -1 store lands in an already flushed slot)
-            R o[K];
-            const R rl = rho2 * kLN2;
+            R o[K], l2[K];
 #pragma unroll
-            for (int j = 0; j < K; ++j) o[j] = fma(N::flg2(q[j]), kLN2, rl);
+            for (int j = 0; j < K; ++j) l2[j] = N::flg2(q[j]);
+            V<R, K>::fma_ss(o, kLN2, l2, rho2 * kLN2);
             SVec<R, K>::st(myB + (t & 3) * K, o);
           }
           if constexpr (PH2) {
             // the pending posterior gamma_{t+1} meets the features of y_{t+1}
             // (the first one is the boundary posterior gamma_{HL-1})
-            stats_step<R, K, CFG>(st, pg, em.em, f0, f1);
-            R Z = R(0);
-#pragma unroll
-            for (int j = 0; j < K; ++j) Z = fma(al[j], q[j], Z);
-            R iz = N::frcp(Z);
+            stats(pg, f0, f1);
+            R iz = N::frcp(V<R, K>::dot(al, q));
             if (sub == 3) iz = (t < 0 && lane == 0) ? R(0) : iz;  // no pair before t = 0
             R ai[K];
+            V<R, K>::mul_s(ai, iz, al);
 #pragma unroll
-            for (int j = 0; j < K; ++j) ai[j] = al[j] * iz;
-#pragma unroll
-            for (int r = 0; r < K; ++r)
-#pragma unroll
-              for (int c = 0; c < K; ++c) X[r][c] = fma(ai[r], w[c], X[r][c]);
-#pragma unroll
-            for (int j = 0; j < K; ++j) pg[j] = ai[j] * q[j];
+            for (int r = 0; r < K; ++r) V<R, K>::fma_s(X[r], ai[r], w, X[r]);
+            V<R, K>::mul(pg, ai, q);
             SVec<R, K>::st(myGb + (t & 3) * K, pg);
             if (sub == 2) {  // t = 0 in the last group
 #pragma unroll
@@ -777,22 +944,22 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
 #pragma unroll
           for (int j = 0; j < K; ++j) bt[j] = q[j];
           rho = rho2;
-          if (rnb_step || (sub == 3 && --gcb == 0)) {
-            if (!rnb_step) gcb = rnb_groups;
-            renorm_vec<R, K>(bt, rho);
-          }
           if constexpr (!PH2) {
             if (t >= HL) park_st(t, bt);
           }
         }
         if (sub == 2) {  // backward slabs [L-4-4g, L-4g) complete
           const int tb = L - 4 - 4 * g;
-          flush(outB, stB, tb);
-          if constexpr (PH2) flush(outG, stGb, tb);
+          if (outB) flush(outB, stB, tb);
+          if constexpr (PH2) {
+            if (outG) flush(outG, stGb, tb);
+          }
         }
       }
-      flush(outA, stA, 4 * g);  // forward slabs [4g, 4g+4) complete
-      if constexpr (PH2) flush(outG, stGf, 4 * g);
+      if (outA) flush(outA, stA, 4 * g);  // forward slabs [4g, 4g+4) complete
+      if constexpr (PH2) {
+        if (outG) flush(outG, stGf, 4 * g);
+      }
       yf = yfn;
       yb = ybn;
       if (two) {
@@ -807,17 +974,22 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
       // boundary: gamma_{HL-1} from alpha~_{HL-1} (av) and beta~_{HL-1} (bt);
       // it is the first pending posterior of the backward direction
       if constexpr (TM) tm_wait_st();
-      R Z = R(0);
-#pragma unroll
-      for (int j = 0; j < K; ++j) Z = fma(av[j], bt[j], Z);
-      const R iz = N::frcp(Z);
-#pragma unroll
-      for (int j = 0; j < K; ++j) pg[j] = av[j] * bt[j] * iz;
+      const R iz = N::frcp(V<R, K>::dot(av, bt));
+      V<R, K>::mul(pg, av, bt);
+      V<R, K>::mul_s(pg, iz, pg);
       SVec<R, K>::st(myGb + 3 * K, pg);
       __syncwarp();
     }
 #pragma unroll 1
     for (int g = NG / 2; g < NG; ++g) group(g, std::true_type{});
+    if constexpr (CFG == kCfgGauss) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        st[0][j][0] = gs0[j];
+        st[0][j][1] = gs1[j];
+        st[0][j][2] = gs2[j];
+      }
+    }
 
     // ===================== per-sequence results =============================
     if (!act) {

@@ -457,32 +457,62 @@ __global__ void __launch_bounds__(256) reduce_mstep_kernel(
     const loghmm_model_t* __restrict__ min_, int64_t nseq, double eps, double nu_ceiling,
     double nu_tol, int max_newton, loghmm_model_t* __restrict__ mout, int32_t* __restrict__ status,
     double* __restrict__ guard, double var_ratio, int do_mstep) {
-  extern __shared__ double tot_s[];
+  extern __shared__ double tot_s[];  // [W1] totals, then [G][CP] group sums
   __shared__ bool last;
-  const int64_t W1 = width + 1;
+  const int W1 = (int)width + 1;
+  // columns are summed CP at a time by thread (g, cc): column c0 + cc of
+  // every G-th row, so each row is read by CP consecutive threads (coalesced)
+  // and every thread has many independent loads in flight; the G group sums
+  // are then added in group order (fixed, bit-reproducible).
+  const int CP = min(W1, (int)blockDim.x);
+  const int G = (int)blockDim.x / CP;
+  const int g = (int)threadIdx.x / CP, cc = (int)threadIdx.x % CP;
+  double* grp = tot_s + W1;
+  auto col_sum = [&](const double* __restrict__ base, int64_t stride, int64_t r0, int64_t r1,
+                     int c, bool is_ll) -> double {
+    double acc = 0.0;
+    int64_t r = r0 + g;
+#pragma unroll 1
+    for (; r + 7 * G < r1; r += 8 * G) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        v[k] = is_ll ? __ldcg(ll + r + k * G) : __ldcg(base + (r + k * G) * stride + c);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[k];
+    }
+    for (; r < r1; r += G) acc += is_ll ? __ldcg(ll + r) : __ldcg(base + r * stride + c);
+    return acc;
+  };
+  // out[c] = sum over rows [r0, r1) of src[., c] (src = partials + ll column, or part)
+  auto reduce_rows = [&](bool from_partials, int64_t r0, int64_t r1, double* out, bool keep) {
+    for (int c0 = 0; c0 < W1; c0 += CP) {
+      const int c = c0 + cc;
+      double acc = 0.0;
+      if (g < G && c < W1)
+        acc = from_partials ? col_sum(partials, width, r0, r1, c, c == W1 - 1)
+                            : col_sum(part, W1, r0, r1, c, false);
+      if (g < G) grp[g * CP + cc] = acc;
+      __syncthreads();
+      if ((int)threadIdx.x < CP && c0 + (int)threadIdx.x < W1) {
+        double s2 = 0.0;
+        for (int k = 0; k < G; ++k) s2 += grp[k * CP + threadIdx.x];
+        out[c0 + threadIdx.x] = s2;
+        if (keep) tot_s[c0 + threadIdx.x] = s2;
+      }
+      __syncthreads();
+    }
+  };
   const int64_t rpb = (B + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(B, r0 + rpb);
-  for (int64_t c = threadIdx.x; c < W1; c += blockDim.x) {
-    double acc = 0.0;
-    if (c < width) {
-      for (int64_t r = r0; r < r1; ++r) acc += partials[r * width + c];
-    } else {
-      for (int64_t r = r0; r < r1; ++r) acc += ll[r];
-    }
-    part[(int64_t)blockIdx.x * W1 + c] = acc;
-  }
+  reduce_rows(true, r0, r1, part + (int64_t)blockIdx.x * W1, false);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int64_t c = threadIdx.x; c < W1; c += blockDim.x) {
-    double acc = 0.0;
-    for (unsigned r = 0; r < gridDim.x; ++r) acc += __ldcg(part + (int64_t)r * W1 + c);
-    totals[c] = acc;
-    tot_s[c] = acc;
-  }
+  reduce_rows(false, 0, gridDim.x, totals, true);
   if (threadIdx.x == 0) *counter = 0u;
   __syncthreads();
   if (do_mstep)
