@@ -349,7 +349,9 @@ def ours(a):
                    "launch": "cuda graph replay" if graph is not None else "eager",
                    "parallelism": f"dp{world} (sequences sharded, statistics all-reduced)" if world > 1 else "single GPU"},
         "roofline": {
-            "bound": "hbm", "kernel": "fb_small_kernel (forward-backward, K=4)",
+            "bound": "hbm",
+            "kernel": ("fb_chunk_kernel (chunk operators + meet-in-the-middle re-sweep, K=4)" if td == torch.float32
+                       else "fb_small_kernel (chunked associative scan, K=4)"),
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src,
             "alg_bytes_per_launch": fb_bytes, "kernel_ms": fb_ms,

@@ -113,6 +113,9 @@ static VitGeom vit_geom(int K, int64_t max_T, int esz = 8, int ns = 2) {
   g.warp_words = (int)(stage_words + (g.global ? 0 : g.plane_words));
   g.warp_words = (g.warp_words + 3) & ~3;
   g.wpb = (int)std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / ((int64_t)g.warp_words * 4)));
+  // warps per CTA: smaller CTAs spread the (one partial wave) Viterbi grid
+  // over more SMs next to the concurrent forward-backward kernel
+  if (const char* env = getenv("LOGHMM_VIT_WPB")) g.wpb = std::max(1, std::min(g.wpb, atoi(env)));
   g.smem = (size_t)g.warp_words * 4 * g.wpb;
   return g;
 }
@@ -480,7 +483,7 @@ int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 
-static constexpr int kReduceBlocks = 128;
+static constexpr int kReduceBlocks = 256;  // upper bound on the reduction grid
 
 size_t loghmm_reduce_workspace_bytes(int64_t B, int64_t width) {
   (void)B;
@@ -502,13 +505,19 @@ int32_t loghmm_reduce_mstep(const double* partials, const double* ll, int64_t B,
   unsigned* counter =
       (unsigned*)((char*)workspace + align256((size_t)kReduceBlocks * (size_t)(width + 1) * 8));
   // totals + one row of column sums per thread group (see the kernel)
-  const size_t smem = (size_t)(width + 1 + 256) * sizeof(double);
+  // 1024 threads = G row groups x (width + 1) columns; about sqrt(B) blocks so
+  // that both reduction levels keep ~B / (G * sqrt(B)) rows per thread (one
+  // batch of independent loads each)
+  constexpr int kRedThreads = 1024;
+  const size_t smem = (size_t)(width + 1 + kRedThreads) * sizeof(double);
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(reduce_mstep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return LOGHMM_ELAUNCH;
-  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(kReduceBlocks, B));
-  reduce_mstep_kernel<<<nb, 256, smem, (cudaStream_t)stream>>>(
+  int64_t nbl = 1;
+  while (nbl * nbl < B) ++nbl;
+  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(kReduceBlocks, nbl));
+  reduce_mstep_kernel<<<nb, kRedThreads, smem, (cudaStream_t)stream>>>(
       partials, ll, B, width, part, counter, totals, model_in, n_sequences, collapse_epsilon,
       nu_ceiling, nu_tol, max_newton, model_out, status, guard_state, var_ratio, do_mstep ? 1 : 0);
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;

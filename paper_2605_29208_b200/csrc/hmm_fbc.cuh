@@ -64,8 +64,9 @@ struct FBCGeom {
   static constexpr int EPU = 16 / (int)sizeof(R);         // elements per unit
   // shared-memory elements per warp: four output stages, plus the parked
   // vectors [L][32][K] for fp64 (fp32 parks them in tensor memory)
+  // (+ [3][32][K] per-lane scratch: entering vector, gamma_0, last gamma)
   static __host__ __device__ int warp_elems(int L) {
-    return 4 * STAGE + (sizeof(R) == 4 ? 0 : L * kWarp * K);
+    return 4 * STAGE + 3 * kWarp * K + (sizeof(R) == 4 ? 0 : L * kWarp * K);
   }
 };
 
@@ -424,7 +425,8 @@ __device__ __forceinline__ void norm_op(R (&Z)[K][K], double& off2) {
 }
 
 template <typename R, int K, int CFG>
-__global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
+__global__ void __launch_bounds__(128)
+    fb_chunk_kernel(const FBCArgs a) {
   typedef Num<R> N;
   typedef CfgTraits<CFG> TR;
   typedef FBCGeom<R, K> G;
@@ -469,7 +471,11 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
     R* stB = stA + G::STAGE;   // log_beta slabs
     R* stGf = stB + G::STAGE;  // gamma slabs, forward direction
     R* stGb = stGf + G::STAGE; // gamma slabs, backward direction
-    R* mypark = stGb + G::STAGE + lane * K;  // fp64: [L][32][K] in shared memory
+    R* aux = stGb + G::STAGE;                 // [3][32][K] per-lane scratch
+    R* myAin = aux + lane * K;                // entering forward vector
+    R* myG0 = aux + kWarp * K + lane * K;     // gamma at t = 0 (lane 0)
+    R* myGl = aux + 2 * kWarp * K + lane * K; // last gamma of the chunk
+    R* mypark = aux + 3 * kWarp * K + lane * K;  // fp64: [L][32][K] in shared memory
     R* myA = stA + lane * G::PITCH;
     R* myB = stB + lane * G::PITCH;
     R* myGf = stGf + lane * G::PITCH;
@@ -497,12 +503,9 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
         Am[i][j] = (R)md->A[i * K + j];
         minA = fmin(Am[i][j], minA);
       }
-    R lpi2[K], pil[K];
+    R lpi2[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      lpi2[j] = (R)(md->log_pi[j] * 1.4426950408889634);
-      pil[j] = (R)md->pi[j];
-    }
+    for (int j = 0; j < K; ++j) lpi2[j] = (R)(md->log_pi[j] * 1.4426950408889634);
     Em2<R, K, CFG> em;
     em.load(md, a.n_streams, a.stream_fams, a.lut, a.lut_n);
     // Pass-1 operator renormalisation every nn steps: its max entry shrinks
@@ -770,11 +773,9 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
     R st[TR::S][K][LOGHMM_NSLOT];
     R gs0[K], gs1[K], gs2[K];  // Gaussian statistics (w, w d, w d^2), packed
     R mu[K];                   // Gaussian means (statistics shift)
-    R g0[K], glast[K], pg[K];
+    R pg[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      g0[i] = R(0);
-      glast[i] = R(0);
       pg[i] = R(0);
       gs0[i] = gs1[i] = gs2[i] = R(0);
       mu[i] = em.em.e0[i].q[0];
@@ -803,6 +804,14 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
     R lam = lane == 0 ? R(0) : (R)lam_in;  // t = 0 uses p = pi (linear, offset 0)
 #pragma unroll
     for (int j = 0; j < K; ++j) av[j] = a_in[j];
+    {
+      R z[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) z[j] = R(0);
+      SVec<R, K>::st(myAin, a_in);
+      SVec<R, K>::st(myG0, z);
+      SVec<R, K>::st(myGl, z);
+    }
     R bt[K];  // backward: beta~_{t+1}
     R rho = (R)rho_ex;
 #pragma unroll
@@ -860,11 +869,7 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
             SVec<R, K>::ld(mypark + i * (kWarp * K), be);
             SVec<R, K>::ld(mypark + ts * (kWarp * K), al);
           }
-          if (sub == 3) {
-            const bool tail = t < 0;
-#pragma unroll
-            for (int j = 0; j < K; ++j) al[j] = tail ? a_in[j] : al[j];
-          }
+          if (sub == 3 && t < 0) SVec<R, K>::ld(myAin, al);  // chunk tail: alpha~_{t0-1}
         }
         // ----------------------- forward step t = i -----------------------
         {
@@ -876,9 +881,10 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
 #pragma unroll
           for (int r = 1; r < K; ++r) V<R, K>::fma_s(p, av[r], Am[r], p);
           if (!PH2 && sub == 0) {
-            const bool first = (g == 0) && (lane == 0);
+            if (g == 0 && lane == 0) {  // t = 0: p = pi (linear), offset 0
 #pragma unroll
-            for (int j = 0; j < K; ++j) p[j] = first ? pil[j] : p[j];
+              for (int j = 0; j < K; ++j) p[j] = (R)__ldg(&md->pi[j]);
+            }
           }
           {
             R o[K], l2[K];
@@ -898,10 +904,7 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
             for (int r = 0; r < K; ++r) V<R, K>::fma_s(X[r], av[r], cv, X[r]);
             SVec<R, K>::st(myGf + sub * K, gg);
             stats(gg, f0, f1);
-            if (sub == 3) {
-#pragma unroll
-              for (int j = 0; j < K; ++j) glast[j] = gg[j];
-            }
+            if (sub == 3) SVec<R, K>::st(myGl, gg);
           }
           V<R, K>::mul(av, p, bh);
           lam += m;
@@ -936,10 +939,7 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
             for (int r = 0; r < K; ++r) V<R, K>::fma_s(X[r], ai[r], w, X[r]);
             V<R, K>::mul(pg, ai, q);
             SVec<R, K>::st(myGb + (t & 3) * K, pg);
-            if (sub == 2) {  // t = 0 in the last group
-#pragma unroll
-              for (int j = 0; j < K; ++j) g0[j] = pg[j];
-            }
+            if (sub == 2) SVec<R, K>::st(myG0, pg);  // t = 0 in the last group
           }
 #pragma unroll
           for (int j = 0; j < K; ++j) bt[j] = q[j];
@@ -1044,6 +1044,10 @@ __global__ void __launch_bounds__(128) fb_chunk_kernel(const FBCArgs a) {
           ++idx;
         }
       // gamma totals over t < T-1 = all-step mass minus the last posterior
+#pragma unroll
+      R glast[K], g0[K];
+      SVec<R, K>::ld(myGl, glast);
+      SVec<R, K>::ld(myG0, g0);
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         const R v = warp_sum(st[0][j][0] - (lane == C - 1 ? glast[j] : R(0)));

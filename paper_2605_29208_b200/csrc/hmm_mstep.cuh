@@ -451,13 +451,13 @@ __global__ void __launch_bounds__(256) mstep_kernel(const loghmm_model_t* __rest
 // partials in block order into totals (also kept in shared memory) and runs
 // the M-step.  `counter` must be zero before the first launch; the last block
 // resets it.
-__global__ void __launch_bounds__(256) reduce_mstep_kernel(
+__global__ void __launch_bounds__(1024) reduce_mstep_kernel(
     const double* __restrict__ partials, const double* __restrict__ ll, int64_t B, int64_t width,
     double* __restrict__ part, unsigned* __restrict__ counter, double* __restrict__ totals,
     const loghmm_model_t* __restrict__ min_, int64_t nseq, double eps, double nu_ceiling,
     double nu_tol, int max_newton, loghmm_model_t* __restrict__ mout, int32_t* __restrict__ status,
     double* __restrict__ guard, double var_ratio, int do_mstep) {
-  extern __shared__ double tot_s[];  // [W1] totals, then [G][CP] group sums
+  extern __shared__ double tot_s[];  // [W1] totals, then [G][CP] group sums (G*CP <= blockDim)
   __shared__ bool last;
   const int W1 = (int)width + 1;
   // columns are summed CP at a time by thread (g, cc): column c0 + cc of
@@ -471,17 +471,17 @@ __global__ void __launch_bounds__(256) reduce_mstep_kernel(
   auto col_sum = [&](const double* __restrict__ base, int64_t stride, int64_t r0, int64_t r1,
                      int c, bool is_ll) -> double {
     double acc = 0.0;
-    int64_t r = r0 + g;
 #pragma unroll 1
-    for (; r + 7 * G < r1; r += 8 * G) {
-      double v[8];
+    for (int64_t r = r0 + g; r < r1; r += 8 * G) {
+      double v[8];  // eight independent (predicated) loads in flight
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        v[k] = is_ll ? __ldcg(ll + r + k * G) : __ldcg(base + (r + k * G) * stride + c);
+      for (int k = 0; k < 8; ++k) {
+        const int64_t rr = r + (int64_t)k * G;
+        v[k] = rr < r1 ? (is_ll ? __ldcg(ll + rr) : __ldcg(base + rr * stride + c)) : 0.0;
+      }
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc += v[k];
     }
-    for (; r < r1; r += G) acc += is_ll ? __ldcg(ll + r) : __ldcg(base + r * stride + c);
     return acc;
   };
   // out[c] = sum over rows [r0, r1) of src[., c] (src = partials + ll column, or part)

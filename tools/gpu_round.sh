@@ -1,6 +1,6 @@
 #!/bin/bash
-# One GPU round trip: parity tests, smoke, bench (fp32 + fp64), ncu launch list
-# and one full capture of the FB and Viterbi kernels.  Writes gpurun_out/.
+# One GPU round trip: parity tests, smoke, bench (fp32 + fp64 + reference arm),
+# ncu launch list of an eager bench step, and full captures of the hot kernels.
 set -x
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi.txt 2>&1
@@ -9,6 +9,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/bench_f32.json 2> gpurun_out/bench_f32.err
 timeout 600 python bench.py --dtype float64 --no-cpu-baseline > gpurun_out/bench_f64.json 2> gpurun_out/bench_f64.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fb_mitm|viterbi" -s 6 -c 3 -o gpurun_out/full_f32 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fb_chunk|viterbi_small|reduce_mstep" -c 3 -o gpurun_out/full_f32 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:"fb_small" -c 1 -o gpurun_out/full_f64 python tools/prof_kernels.py --dtype float64 --reps 1 --only fb > gpurun_out/ncu_full64.log 2>&1
 ls -la gpurun_out
