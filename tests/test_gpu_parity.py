@@ -140,10 +140,52 @@ def _random_gauss_model(rng, K):
 
 @pytest.fixture(params=["auto", "pair"])
 def vit_algo(request, monkeypatch):
-    """Run a test under both Viterbi layouts (two-lane for K<=4, K-lane)."""
-    if request.param == "pair":
-        monkeypatch.setenv("LOGHMM_VIT_ALGO", "pair")
+    """Run a test under both Viterbi layouts (K lanes per sequence by default,
+    two lanes for K <= 4 on request)."""
+    if request.param != "auto":
+        monkeypatch.setenv("LOGHMM_VIT_ALGO", request.param)
+    else:
+        monkeypatch.delenv("LOGHMM_VIT_ALGO", raising=False)
     return request.param
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+@pytest.mark.parametrize("T", [4, 8, 36, 1000, 1024])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_viterbi_equal_length_bitexact(K, T, dtype, vit_algo):
+    """Equal-length batches: path, backpointers and log joint bit-identical
+    to the reference restatement, including exact ties (a model with a
+    duplicated state, so candidates tie every step and the first index must
+    win)."""
+    rng = np.random.default_rng(1000 * K + T)
+    m = _random_gauss_model(rng, K)
+    if K >= 3:  # duplicate state 0 into state 2: candidate ties every step
+        mus = [d.mu for d in m.emissions]
+        sds = [d.sigma for d in m.emissions]
+        mus[2], sds[2] = mus[0], sds[0]
+        A = np.array(m.transitions)
+        A[2, :] = A[0, :]
+        A[:, 2] = A[:, 0]
+        A /= A.sum(1, keepdims=True)
+        pi = np.array(m.initial)
+        pi[2] = pi[0]
+        pi /= pi.sum()
+        m = H.HmmModel(pi, A, tuple(H.Gaussian(a, b) for a, b in zip(mus, sds)))
+    seqs = [rng.normal(0, 3, T) for _ in range(37)]
+    out = H.viterbi_batch(m, seqs, dtype=dtype, back=True)
+    path = out.path.cpu().numpy()
+    back = out.back.cpu().numpy()
+    lj = out.log_joint.cpu().numpy()
+    lp, la = O.model_tables(m.initial, m.transitions)
+    R = np.float32 if dtype == "float32" else np.float64
+    for b, y in enumerate(seqs):
+        yy = y.astype(R)
+        lb = O.emission_matrix(to_tuples(m), yy, R)
+        p, j, bk = O.viterbi(lp.astype(R), la.astype(R), lb, R)
+        s = slice(b * T, (b + 1) * T)
+        assert np.array_equal(path[s], p), (K, T, b)
+        assert np.array_equal(back[s].astype(np.int64), bk), (K, T, b)
+        assert lj[b] == j
 
 
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 5, 8])
