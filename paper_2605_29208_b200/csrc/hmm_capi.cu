@@ -193,7 +193,7 @@ static int fbc_chunk_len(int64_t T) {
 }
 
 static int fbc_warp_elems(int K, int esz, int L) {
-#define C_(KK) case KK: return esz == 8 ? fb_chunk_warp_elems<double, KK>(L) : fb_chunk_warp_elems<float, KK>(L);
+#define C_(KK) case KK: return esz == 4 ? fb_chunk_warp_elems<float, KK>(L) : 0;
   switch (K) { C_(2) C_(3) C_(4) C_(5) C_(6) C_(7) C_(8) default: return 0; }
 #undef C_
 }
@@ -209,7 +209,7 @@ static int fbc_tm_cols(int K, int L) {
 constexpr int kFbcWarpsPerBlock = 4;  // one warpgroup (kFbcWarps)
 constexpr size_t kFbcMaxWarpBytes = 100 * 1024;
 
-static bool use_fbc(int K, int64_t B, int64_t N, int64_t max_T, int esz, bool xi, int* L_out,
+static bool use_fbc(int K, int n_streams, int64_t B, int64_t N, int64_t max_T, int esz, bool xi, int* L_out,
                     size_t* warp_bytes) {
   const char* env = getenv("LOGHMM_FB_ALGO");
   if (env && strcmp(env, "chunked") == 0) return false;
@@ -219,6 +219,7 @@ static bool use_fbc(int K, int64_t B, int64_t N, int64_t max_T, int esz, bool xi
   if (K < 2 || K > 8 || xi || max_T < 8 || N != B * max_T || max_T > INT32_MAX) return false;
   const int L = fbc_chunk_len(max_T);
   if (L == 0) return false;
+  (void)n_streams;
   const size_t wb = (size_t)fbc_warp_elems(K, esz, L) * esz;
   if (wb > kFbcMaxWarpBytes) return false;
   if (esz == 4 && fbc_tm_cols(K, L) > 256) return false;  // tensor-memory park
@@ -335,7 +336,7 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
   cudaError_t e;
   int fbcL = 0;
   size_t fbcW = 0;
-  if (use_fbc(K, B, N, max_T, esz, xi != nullptr, &fbcL, &fbcW)) {
+  if (use_fbc(K, h_desc->n_streams, B, N, max_T, esz, xi != nullptr, &fbcL, &fbcW)) {
     FBCArgs c{};
     c.model = model;
     c.y0 = a.y0;
@@ -360,8 +361,8 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
     const int wpb = esz == 4 ? kFbcWarpsPerBlock
                              : (int)std::max<size_t>(1, std::min<size_t>(kFbcWarpsPerBlock, (220 * 1024) / fbcW));
     dim3 grid((unsigned)((B + wpb - 1) / wpb)), block(32 * wpb);
-    e = dtype == LOGHMM_F64 ? dispatch_fb_chunk<double>(K, c, cfg, grid, block, fbcW * wpb, st)
-                            : dispatch_fb_chunk<float>(K, c, cfg, grid, block, fbcW * wpb, st);
+    // (instantiated for fp32 only; use_fbc() keeps fp64 on the chunked scan)
+    e = dispatch_fb_chunk<float>(K, c, cfg, grid, block, fbcW * wpb, st);
   } else if (K <= 8) {
     FBGeom g = fb_geom(K, esz, h_desc->n_streams, max_T);
     a.L_align = g.L_align;

@@ -1,0 +1,9 @@
+#!/bin/bash
+# A/B the pipeline bench between library builds in abtest/<name>/ (interleaved runs).
+mkdir -p gpurun_out
+for rep in 1 2 3; do
+  for v in "$@"; do
+    LOGHMM_B200_LIB=$PWD/abtest/$v/libloghmm_b200.so timeout 300 python bench.py --no-cpu-baseline --steps 30 > gpurun_out/ab_$v.json 2>&1
+    python3 -c "import json; d=json.loads(open('gpurun_out/ab_$v.json').read().strip().splitlines()[-1]); print('$v', round(d['ms_per_step']*1000,1), round(d['roofline']['kernel_ms']*1000,1), round(d['pipeline_roofline']['viterbi_kernel_ms']*1000,1))"
+  done
+done
