@@ -9,6 +9,11 @@ One ``run`` enqueues, on the caller's current stream:
          -> loghmm_mstep (-> loghmm_student_guard for Student-t states)
 No host synchronisation inside ``run``; ``fetch`` reads back the small
 results (total log-likelihood, the updated model block) like a user would.
+
+``run_from_host`` is the same step fed from pinned host memory: the batch is
+cut into slices of whole sequences, slice s+1's host-to-device copy runs on
+a copy stream while slices <= s are in the forward-backward / Viterbi
+kernels, and the statistics reduction + M-step runs once over all slices.
 """
 
 from __future__ import annotations
@@ -78,6 +83,8 @@ class Pipeline:
         var_fams = (_native.FAM["gaussian"], _native.FAM["gamma"], _native.FAM["student_t"])
         self.var_streams = [s for s in range(self.ns)
                             if any(int(fams[s, j]) in var_fams for j in range(K))]
+        self.s_copy = torch.cuda.Stream(device=dev)
+        self._slices = {}
         # per-kernel CUDA events (recorded on the stream each kernel runs on)
         self.ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for k in ("fb", "vit")}
@@ -135,6 +142,11 @@ class Pipeline:
             launch_fb()
         main.wait_stream(self.s_fb)
         main.wait_stream(self.s_vit)
+        self._tail()
+
+    def _tail(self) -> None:
+        """Statistics reduction (+ all-reduce across ranks), M-step and the
+        exact second passes, on the current stream."""
         if self.pg is None:
             # single rank: block reduction and M-step in one launch
             engine.reduce_mstep(self.fb.partials, self.fb.ll, self.totals, self.dm, self.B,
@@ -152,6 +164,62 @@ class Pipeline:
         for s in self.student_streams:
             engine.student_guard(self.batch, self.dm_next, self.fb.gamma, s, 2, self.guard,
                                  self.status, self.need_more)
+
+    def _slice_plan(self, n: int):
+        """Per-slice views (batch, FB outputs, Viterbi outputs) of n equal
+        slices of whole sequences."""
+        if n in self._slices:
+            return self._slices[n]
+        B, T = self.B, self.T
+        bounds = [B * i // n for i in range(n + 1)]
+        plans = []
+        for i in range(n):
+            b0, b1 = bounds[i], bounds[i + 1]
+            if b1 <= b0:
+                continue
+            r0, r1 = b0 * T, b1 * T
+            off = np.arange(b1 - b0 + 1, dtype=np.int64) * T
+            batch = engine.Batch(self.y0[r0:r1], self.y1[r0:r1] if self.y1 is not None else None,
+                                 torch.from_numpy(off).to(self.dev), off, self.td)
+            fb = engine.FBOutputs(
+                log_alpha=self.fb.log_alpha[r0:r1] if self.fb.log_alpha is not None else None,
+                log_beta=self.fb.log_beta[r0:r1] if self.fb.log_beta is not None else None,
+                gamma=self.fb.gamma[r0:r1], xi=None, ll=self.fb.ll[b0:b1],
+                partials=self.fb.partials[b0:b1], flags=self.fb.flags[b0:b1])
+            vit = engine.VitOutputs(path=self.vit.path[r0:r1], log_joint=self.vit.log_joint[b0:b1],
+                                    back=None, flags=self.vit.flags[b0:b1])
+            plans.append((r0, r1, batch, fb, vit, torch.cuda.Event()))
+        self._slices[n] = plans
+        return plans
+
+    def run_from_host(self, y_host, slices: int = 8) -> None:
+        """One step whose observations come from (pinned) host memory, with
+        the host-to-device copy of each slice overlapped with the kernels of
+        the slices before it."""
+        y = torch.as_tensor(y_host)
+        ys = [y.reshape(-1)] if self.ns == 1 else [y[..., 0].reshape(-1), y[..., 1].reshape(-1)]
+        dst = [self.y0] if self.ns == 1 else [self.y0, self.y1]
+        main = torch.cuda.current_stream(self.dev)
+        plans = self._slice_plan(slices)
+        self.s_copy.wait_stream(main)
+        self.s_fb.wait_stream(main)
+        self.s_vit.wait_stream(main)
+        with torch.cuda.stream(self.s_copy):
+            for r0, r1, _, _, _, ev in plans:
+                for d, src in zip(dst, ys):
+                    d[r0:r1].copy_(src[r0:r1], non_blocking=True)
+                ev.record(self.s_copy)
+        for _, _, batch, fb, vit, ev in plans:
+            self.s_vit.wait_event(ev)
+            with torch.cuda.stream(self.s_vit):
+                engine.viterbi(batch, self.dm, out=vit, workspace=self.ws_vit)
+            self.s_fb.wait_event(ev)
+            with torch.cuda.stream(self.s_fb):
+                engine.forward_backward(batch, self.dm, stats=True, out=fb, workspace=self.ws_fb)
+        main.wait_stream(self.s_copy)
+        main.wait_stream(self.s_fb)
+        main.wait_stream(self.s_vit)
+        self._tail()
 
     def _world(self) -> int:
         import torch.distributed as dist

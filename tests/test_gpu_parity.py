@@ -531,3 +531,31 @@ def test_exact_gaussian_emission_wide_range(dtype):
         ref = O.emission_matrix([("gaussian", mu, sigma)], y, R)
         got = np.asarray(lb).reshape(-1)
         assert np.array_equal(got, ref[:, 0]), (mu, sigma, int((got != ref[:, 0]).sum()))
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_pipeline_host_slices_match_device_run(dtype):
+    """Pipeline.run_from_host (sliced H2D overlapped with the kernels) gives
+    the same statistics, log-likelihood and updated model as run() on the
+    same observations already on the device."""
+    from paper_2605_29208_b200.pipeline import Pipeline
+
+    cfg = make_config("c2", B=96, T=256)
+    td = torch.float32 if dtype == "float32" else torch.float64
+    y_host = torch.from_numpy(cfg.data).to(td).pin_memory()
+    p = Pipeline(cfg.init, cfg.B, cfg.T, dtype)
+    p.load(y_host)
+    p.run()
+    torch.cuda.synchronize()
+    ref_tot = p.totals.clone()
+    ref_model = p.dm_next.buf.clone()
+    ref_path = p.vit.path.clone()
+    ref_gamma = p.fb.gamma.clone()
+    for slices in (1, 3, 8):
+        p.y0.zero_()
+        p.run_from_host(y_host, slices=slices)
+        torch.cuda.synchronize()
+        assert torch.equal(p.totals, ref_tot), slices
+        assert torch.equal(p.dm_next.buf, ref_model), slices
+        assert torch.equal(p.vit.path, ref_path), slices
+        assert torch.equal(p.fb.gamma, ref_gamma), slices
