@@ -358,8 +358,9 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
     c.tm_cols = esz == 4 ? fbc_tm_cols(K, fbcL) : 0;
     // fp32: one warpgroup per CTA (tensor-memory lane quadrants); fp64: as
     // many warps as the shared-memory park allows, up to four
-    const int wpb = esz == 4 ? kFbcWarpsPerBlock
-                             : (int)std::max<size_t>(1, std::min<size_t>(kFbcWarpsPerBlock, (220 * 1024) / fbcW));
+    int wpb = esz == 4 ? kFbcWarpsPerBlock
+                       : (int)std::max<size_t>(1, std::min<size_t>(kFbcWarpsPerBlock, (220 * 1024) / fbcW));
+    if (const char* env = getenv("LOGHMM_FBC_WPB")) wpb = std::max(1, std::min(4, atoi(env)));
     dim3 grid((unsigned)((B + wpb - 1) / wpb)), block(32 * wpb);
     // (instantiated for fp32 only; use_fbc() keeps fp64 on the chunked scan)
     e = dispatch_fb_chunk<float>(K, c, cfg, grid, block, fbcW * wpb, st);
