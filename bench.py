@@ -34,6 +34,12 @@ sys.path.insert(0, str(ROOT))
 METRIC = "F-B+Viterbi state-steps/s (B·T·K) at B=4096,T=1024,K=4; % of HBM roofline"
 UNIT = "state-steps/s"
 WORKLOAD = "c2: B=4096 T=1024 K=4 Gaussian HMM; FB(log_alpha,log_beta,gamma,xi/stats)+Viterbi(path)+1 Baum-Welch M-step"
+WORKLOADS = {
+    "c2": WORKLOAD,
+    "c3": "c3: B=1024 T=2048 K=3 Student-t HMM; FB+Viterbi+1 Baum-Welch M-step (ECME, likelihood guard)",
+    "c4": "c4: B=2048 T=2000 K=3 Gamma+von Mises joint HMM; FB+Viterbi+1 Baum-Welch M-step (Gamma NR, kappa Newton)",
+    "c5": "c5: B=64 T=65536 K=64 Poisson HMM (banded A); FB+Viterbi+1 Baum-Welch M-step",
+}
 
 
 def parse():
@@ -43,8 +49,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
-    ap.add_argument("--B", type=int, default=4096)
-    ap.add_argument("--T", type=int, default=1024)
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
+                    help="BASELINE config (c2 is the headline; c3-c5 are auxiliary lines)")
+    ap.add_argument("--B", type=int, default=None)
+    ap.add_argument("--T", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -64,6 +72,20 @@ def peaks():
 # ---------------------------------------------------------------------------
 # CPU reference (the oracle port of the reference algorithm; test infra)
 # ---------------------------------------------------------------------------
+def oracle_spec(model):
+    """Emission spec tuples of a model for the oracle (family, *params)."""
+    from paper_2605_29208_b200 import HmmModel, Joint
+
+    out = []
+    for d in model.emissions:
+        if isinstance(d, Joint):
+            out.append(("joint", oracle_spec(HmmModel([1.0], [[1.0]], (d.first,)))[0],
+                        oracle_spec(HmmModel([1.0], [[1.0]], (d.second,)))[0]))
+        else:
+            out.append((d.family,) + tuple(d.params().values()))
+    return out
+
+
 def _cpu_seq(args):
     import loghmm_oracle as O
 
@@ -85,14 +107,15 @@ def cpu_reference_run(cfg, n_seq, pool):
     import loghmm_oracle as O
 
     m = cfg.init
-    ems = [("gaussian", d.mu, d.sigma) for d in m.emissions]
+    ems = oracle_spec(m)
     seqs = [cfg.data[b % cfg.B] for b in range(n_seq)]
     t0 = time.perf_counter()
     res = pool.map(_cpu_seq, [(y, m.initial, m.transitions, ems) for y in seqs])
     G = np.concatenate([r[0] for r in res])
     Y = np.concatenate(seqs)
     for j, fam in enumerate(ems):
-        O.fit(fam, Y, G[:, j])
+        if fam[0] in ("gaussian", "poisson", "gamma", "von_mises", "student_t"):
+            O.fit(fam, Y, G[:, j])
     return time.perf_counter() - t0
 
 
@@ -111,7 +134,7 @@ def reference_arm(a):
         return
     from paper_2605_29208_b200.configs import make_config
 
-    cfg = make_config("c2", B=64, T=a.T)
+    cfg = make_config(a.config, B=64, T=a.T)
     pool, cores = cpu_pool()
     # size each step so the whole --warmup + --steps run takes ~2 minutes
     probe = cpu_reference_run(cfg, cores, pool)
@@ -125,7 +148,7 @@ def reference_arm(a):
         tot += cpu_reference_run(cfg, n_seq, pool)
     pool.close()
     K = cfg.K
-    val = a.steps * n_seq * a.T * K / tot
+    val = a.steps * n_seq * cfg.T * K / tot
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -140,10 +163,10 @@ def reference_arm(a):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (BASELINE config 2 draw, seed 0)",
-        "config": {"workload": WORKLOAD, "B": 4096, "T": a.T, "K": K,
-                   "sample_per_step": f"{n_seq} sequences x T={a.T}"},
+        "config": {"workload": WORKLOADS[a.config], "B": make_config(a.config).B if a.config != "c2" else 4096,
+                   "T": cfg.T, "K": K, "sample_per_step": f"{n_seq} sequences x T={cfg.T}"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{n_seq} sequences of config 2 per step (reference E-step + Viterbi per sequence over {cores} processes, pooled M-step)"},
+                         "sample": f"{n_seq} sequences of config {a.config[1]} per step (reference E-step + Viterbi per sequence over {cores} processes, pooled M-step)"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -218,7 +241,7 @@ def ours(a):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist.group.WORLD
-    cfg = make_config("c2", B=a.B, T=a.T, seed=rank)  # weak scaling: each rank its own batch
+    cfg = make_config(a.config, B=a.B, T=a.T, seed=rank)  # weak scaling: each rank its own batch
     B, T, K = cfg.B, cfg.T, cfg.K
     td = torch.float32 if a.dtype == "float32" else torch.float64
     esz = 4 if td == torch.float32 else 8
@@ -353,14 +376,15 @@ def ours(a):
     peak, peak_src = peaks()
     fb_ms = statistics.mean(kfb)
     vit_ms = statistics.mean(kvit)
-    fb_bytes = B * T * (esz + 3 * K * esz)  # y read once; log_alpha, log_beta, gamma written
-    m1_bytes = B * T * (esz + 3 * K * esz + 8)  # + int64 Viterbi path
+    ns = cfg.init.n_streams
+    fb_bytes = B * T * (ns * esz + 3 * K * esz)  # y read once; log_alpha, log_beta, gamma written
+    m1_bytes = B * T * (ns * esz + 3 * K * esz + 8)  # + int64 Viterbi path
     achieved = fb_bytes / (fb_ms / 1000.0) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "fb_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(a.dtype)
+            traffic = json.loads(tp.read_text()).get(a.dtype) if a.config == "c2" else None
         except Exception:
             traffic = None
     line = {
@@ -376,13 +400,15 @@ def ours(a):
         "vs_baseline": None,
         "dtype": "f32" if td == torch.float32 else "f64",
         "data": "synthetic (BASELINE config 2 draw: Dirichlet transitions, means -3,-1,1,3, std U[0.5,1.5]; seed = rank)",
-        "config": {"workload": WORKLOAD, "B": B, "T": T, "K": K, "l2": "flushed (256 MiB write) between timed steps",
+        "config": {"workload": WORKLOADS[a.config], "B": B, "T": T, "K": K, "l2": "flushed (256 MiB write) between timed steps",
                    "launch": "cuda graph replay" if graph is not None else "eager",
                    "parallelism": f"dp{world} (sequences sharded, statistics all-reduced)" if world > 1 else "single GPU"},
         "roofline": {
             "bound": "hbm",
-            "kernel": ("fb_chunk_kernel (chunk operators + meet-in-the-middle re-sweep, K=4)" if td == torch.float32
-                       else "fb_small_kernel (chunked associative scan, K=4)"),
+            "kernel": (f"fb_large_kernel (K={K})" if K > 8 else
+                       f"fb_chunk_kernel (chunk operators + meet-in-the-middle re-sweep, K={K})"
+                       if td == torch.float32 and T % 8 == 0 else
+                       f"fb_small_kernel (chunked associative scan, K={K})"),
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src,
             "alg_bytes_per_launch": fb_bytes, "kernel_ms": fb_ms,
@@ -401,14 +427,14 @@ def ours(a):
     }
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         pool, cores = cpu_pool()
-        cpu_cfg = make_config("c2", B=64, T=T)
+        cpu_cfg = make_config(a.config, B=min(64, B), T=T)
         probe = cpu_reference_run(cpu_cfg, cores, pool)
         n_seq = int(max(cores, min(512, cores * a.cpu_seconds / max(probe, 1e-3))))
         t = cpu_reference_run(cpu_cfg, n_seq, pool)
         pool.close()
         line["cpu_baseline"] = {
             "value": n_seq * T * K / t, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{n_seq} sequences of config 2 (T={T}, K={K}): reference E-step + Viterbi per sequence over {cores} processes + pooled M-step, {t:.1f} s",
+            "sample": f"{n_seq} sequences of config {a.config[1]} (T={T}, K={K}): reference E-step + Viterbi per sequence over {cores} processes + pooled M-step, {t:.1f} s",
         }
     print(json.dumps(line), flush=True)
     if pg is not None:

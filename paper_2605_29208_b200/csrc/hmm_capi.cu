@@ -377,7 +377,8 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
                             : dispatch_fb_small<float>(K, a, cfg, g.global, grid, block, g.smem, st);
   } else {
     const int threads = 32 * ((K + 31) / 32);
-    const size_t smem = (size_t)(2 * K * K + K + 32) * esz;
+    // A (padded pitch K + 1), vector, reduction scratch, xi accumulators, alpha~_{t-1}
+    const size_t smem = (size_t)(K * (K + 1) + K + 32 + K * K + K) * esz;
     if (dtype == LOGHMM_F64) {
       cudaFuncSetAttribute(fb_large_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       fb_large_kernel<double><<<(unsigned)B, threads, smem, st>>>(a, K);

@@ -56,9 +56,13 @@ template <typename R>
 __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
   typedef Num<R> N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* As = reinterpret_cast<R*>(smem_raw);  // K*K
-  R* av = As + K * K;                      // K (current vector)
+  // A with a padded row pitch (K + 1): row reads A[j][.] across threads j
+  // and column reads A[.][j] are both bank-conflict free
+  const int AP = K + 1;
+  R* As = reinterpret_cast<R*>(smem_raw);  // K * AP
+  R* av = As + K * AP;                     // K (current vector)
   R* red = av + K;                         // 32
+  R* apv = red + 32 + K * K;               // K (alpha~_{t-1}, backward sweep)
   const int tid = threadIdx.x;
   const int nw = blockDim.x >> 5;
   const int64_t b = blockIdx.x;
@@ -68,7 +72,7 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
   const bool act = tid < K;
   const int j = act ? tid : 0;
   const loghmm_model_t* md = a.model;
-  for (int e = tid; e < K * K; e += blockDim.x) As[e] = (R)md->A[e];
+  for (int e = tid; e < K * K; e += blockDim.x) As[(e / K) * AP + e % K] = (R)md->A[e];
   const EmP<R> p0 = load_emission<R>(md->em[0][j]);
   EmP<R> p1;
   const bool two = a.n_streams > 1;
@@ -98,8 +102,13 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
     if (t == 0) {
       u = lpi + lb;
     } else {
-      R acc = R(0);
-      for (int i = 0; i < K; ++i) acc = fma(av[i], As[i * K + j], acc);
+      R c4[4] = {R(0), R(0), R(0), R(0)};  // four independent chains
+      int i = 0;
+      for (; i + 3 < K; i += 4)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c4[q] = fma(av[i + q], As[(i + q) * AP + j], c4[q]);
+      for (; i < K; ++i) c4[0] = fma(av[i], As[i * AP + j], c4[0]);
+      const R acc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
       u = (acc > R(0) ? N::flog(acc) : N::ninf()) + lb;
     }
     if (act && outA) outA[(int64_t)t * K + j] = (R)lam + u;
@@ -161,21 +170,31 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
     const R M = block_max(u, red, nw);
     const bool fin = M > N::ninf();
     const R w = (act && fin) ? N::fexp(u - M) : R(0);
-    if (act) wv[j] = w;
+    const R ap = act ? aws[(int64_t)(t - 1) * K + j] : R(0);
+    if (act) {
+      wv[j] = w;
+      apv[j] = ap;  // alpha~_{t-1}, read by every thread below
+    }
     __syncthreads();
     R acc = R(0);
-    if (act)
-      for (int jj = 0; jj < K; ++jj) acc = fma(As[j * K + jj], wv[jj], acc);
+    if (act) {
+      R c4[4] = {R(0), R(0), R(0), R(0)};
+      int jj = 0;
+      for (; jj + 3 < K; jj += 4)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c4[q] = fma(As[j * AP + jj + q], wv[jj + q], c4[q]);
+      for (; jj < K; ++jj) c4[0] = fma(As[j * AP + jj], wv[jj], c4[0]);
+      acc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+    }
     // xi_{t-1}(i, j) = a_{t-1}[i] A_ij w_j / Z, Z = sum_i a_{t-1}[i] q_i
-    const R ap = act ? aws[(int64_t)(t - 1) * K + j] : R(0);
     const R Z = block_sum(ap * acc, red, nw);
     const R iz = R(1) / Z;
     // thread j (as column) accumulates X[i][j] += a_i/Z * w_j
     if (act) {
+      const R wz = w * iz;
       for (int i = 0; i < K; ++i) {
-        const R ai = aws[(int64_t)(t - 1) * K + i] * iz;
-        X[i * K + j] = fma(ai, w, X[i * K + j]);
-        if (outX) outX[((int64_t)(t - 1) * K + i) * K + j] = ai * As[i * K + j] * w;
+        X[i * K + j] = fma(apv[i], wz, X[i * K + j]);
+        if (outX) outX[((int64_t)(t - 1) * K + i) * K + j] = apv[i] * iz * As[i * AP + j] * w;
       }
     }
     const R lq = acc > R(0) ? N::flog(acc) : N::ninf();
@@ -193,7 +212,7 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
   if (a.partials) {
     double* row = a.partials + b * a.stats_width;
     if (act) {
-      for (int i = 0; i < K; ++i) row[i * K + j] = (double)X[i * K + j] * (double)As[i * K + j];
+      for (int i = 0; i < K; ++i) row[i * K + j] = (double)X[i * K + j] * (double)As[i * AP + j];
       row[K * K + j] = (double)gtot;
       row[K * K + K + j] = (double)g0;
       for (int s = 0; s < 2; ++s)
