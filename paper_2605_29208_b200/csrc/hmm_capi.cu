@@ -260,7 +260,7 @@ int64_t loghmm_stats_width(int32_t K, int32_t n_streams) {
 size_t loghmm_fb_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N, int64_t max_T) {
   (void)B;
   const int esz = dtype == LOGHMM_F64 ? 8 : 4;
-  if (K > 8) return align256((size_t)N * K * esz);
+  if (K > 8) return 2 * align256((size_t)N * K * esz);  // alpha~ store + precomputed log b
   FBGeom g = fb_geom(K, esz, 2, max_T);
   return align256((size_t)B * g.Lmax * kWarp * K * esz);
 }
@@ -379,12 +379,19 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
     const int threads = 32 * ((K + 31) / 32);
     // A (padded pitch K + 1), vector, reduction scratch, xi accumulators, alpha~_{t-1}
     const size_t smem = (size_t)(K * (K + 1) + K + 32 + K * K + K) * esz;
+    // log b for the whole batch first (fully parallel), then the sweeps
+    void* lbw = (char*)workspace + align256((size_t)N * K * esz);
+    const int64_t eblocks = std::min<int64_t>((N + 255) / 256, 148 * 16);
     if (dtype == LOGHMM_F64) {
+      emission_kernel<double><<<(unsigned)eblocks, 256, 0, st>>>(
+          model, (const double*)y0, (const double*)a.y1, N, K, lgamma_lut, lut_n, (double*)lbw);
       cudaFuncSetAttribute(fb_large_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fb_large_kernel<double><<<(unsigned)B, threads, smem, st>>>(a, K);
+      fb_large_kernel<double><<<(unsigned)B, threads, smem, st>>>(a, K, (const double*)lbw);
     } else {
+      emission_kernel<float><<<(unsigned)eblocks, 256, 0, st>>>(
+          model, (const float*)y0, (const float*)a.y1, N, K, lgamma_lut, lut_n, (float*)lbw);
       cudaFuncSetAttribute(fb_large_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fb_large_kernel<float><<<(unsigned)B, threads, smem, st>>>(a, K);
+      fb_large_kernel<float><<<(unsigned)B, threads, smem, st>>>(a, K, (const float*)lbw);
     }
     e = cudaGetLastError();
   }

@@ -2,7 +2,9 @@
 //
 // One CTA per sequence, one thread per state.  The transition matrix is
 // staged once in shared memory; the state vector is exchanged through shared
-// memory with one barrier per step.  This is the straightforward sequential
+// memory with one barrier per step; the emission log-densities are computed
+// for the whole batch beforehand (emission_kernel, fully parallel) so the
+// sequential sweeps only load them, one step ahead.  This is the straightforward sequential
 // sweep over T (inference.py:129-146, 191-210); the parallel-over-T scan of
 // hmm_fb.cuh costs K^3 per step and does not pay at K=64.
 #pragma once
@@ -37,23 +39,20 @@ __device__ __forceinline__ R block_sum(R v, R* red, int nw) {
   return m;
 }
 
-// Runtime-K version of the fast emission for state j.
+// Observation features needed by the E-step statistics only (no lgamma LUT).
 template <typename R>
-__device__ __forceinline__ R large_logb(const EmP<R>& p0, const EmP<R>& p1, bool two, R y0, R y1,
-                                        const double* lut, int lut_n, bool& oob,
-                                        ObsFeat<R>& f0, ObsFeat<R>& f1) {
-  obs_features<R, kCfgMixed>(f0, y0, lut, lut_n, oob, 1 << p0.fam);
-  R v = fast_logb_rt<R>(p0, f0);
-  if (two) {
-    obs_features<R, kCfgMixed>(f1, y1, lut, lut_n, oob, 1 << p1.fam);
-    v += fast_logb_rt<R>(p1, f1);
-  }
-  return v;
+__device__ __forceinline__ void stat_features(ObsFeat<R>& f, R y, int fam) {
+  f.y = y;
+  if (fam == LOGHMM_FAM_GAMMA) f.logy = y > R(0) ? Num<R>::alog(y) : Num<R>::ninf();
+  if (fam == LOGHMM_FAM_VON_MISES) Num<R>::asincos(y, &f.siny, &f.cosy);
+  if (fam == LOGHMM_FAM_POISSON) f.pois_ok = (y >= R(0)) && (floor(y) == y);
 }
 
-// blockDim.x = 32 * ceil(K/32); thread j < K owns state j.
+// blockDim.x = 32 * ceil(K/32); thread j < K owns state j.  The emission
+// log-densities come precomputed ([N, K], emission_kernel) and every per-step
+// load (log b, y, alpha~) is issued one step ahead, off the recursion chain.
 template <typename R>
-__global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
+__global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, const R* __restrict__ lbws) {
   typedef Num<R> N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // A with a padded row pitch (K + 1): row reads A[j][.] across threads j
@@ -93,11 +92,18 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
   // forward
   double lam = 0.0;
   R a_j = R(0);
+  const R* __restrict__ lbs = lbws + start * K;
+  R lbn = (act && T > 0) ? lbs[j] : N::ninf();
+  R yn0 = T > 0 ? y0g[0] : R(0), yn1 = (two && T > 0) ? y1g[0] : R(0);
   for (int t = 0; t < T; ++t) {
-    ObsFeat<R> f0, f1;
-    const R v0 = y0g[t], v1 = two ? y1g[t] : R(0);
+    const R v0 = yn0, v1 = yn1;
+    const R lb = lbn;
+    if (t + 1 < T) {  // prefetch step t + 1
+      lbn = act ? lbs[(int64_t)(t + 1) * K + j] : N::ninf();
+      yn0 = y0g[t + 1];
+      if (two) yn1 = y1g[t + 1];
+    }
     if (isnan(v0) || isnan(v1)) nan_seen = true;
-    const R lb = act ? large_logb<R>(p0, p1, two, v0, v1, a.lut, a.lut_n, oob, f0, f1) : N::ninf();
     R u;
     if (t == 0) {
       u = lpi + lb;
@@ -140,12 +146,21 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
     if (act) X[i * K + j] = R(0);
   R r = R(0);  // log beta~ at current t (max 0)
   double rho = 0.0;
+  R bl = (act && T > 0) ? lbs[(int64_t)(T - 1) * K + j] : N::ninf();
+  R by0 = T > 0 ? y0g[T - 1] : R(0), by1 = (two && T > 0) ? y1g[T - 1] : R(0);
+  R bat = (act && T > 0) ? aws[(int64_t)(T - 1) * K + j] : R(0);
   for (int t = T - 1; t >= 0; --t) {
+    const R v0 = by0, v1 = by1, lb = bl, at = bat;
+    if (t >= 1) {  // prefetch step t - 1 (its alpha~ is also this step's a_{t-1})
+      bl = act ? lbs[(int64_t)(t - 1) * K + j] : N::ninf();
+      by0 = y0g[t - 1];
+      if (two) by1 = y1g[t - 1];
+      bat = act ? aws[(int64_t)(t - 1) * K + j] : R(0);
+    }
     ObsFeat<R> f0, f1;
-    const R v0 = y0g[t], v1 = two ? y1g[t] : R(0);
-    const R lb = act ? large_logb<R>(p0, p1, two, v0, v1, a.lut, a.lut_n, oob, f0, f1) : N::ninf();
+    stat_features<R>(f0, v0, p0.fam);
+    if (two) stat_features<R>(f1, v1, p1.fam);
     // gamma at t: a_t * exp(r)
-    const R at = act ? aws[(int64_t)t * K + j] : R(0);
     const R q = act ? N::fexp(r) : R(0);
     const R gz = block_sum(at * q, red, nw);
     const R gj = at * q / gz;
@@ -170,7 +185,7 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K) {
     const R M = block_max(u, red, nw);
     const bool fin = M > N::ninf();
     const R w = (act && fin) ? N::fexp(u - M) : R(0);
-    const R ap = act ? aws[(int64_t)(t - 1) * K + j] : R(0);
+    const R ap = bat;  // alpha~_{t-1}, prefetched above
     if (act) {
       wv[j] = w;
       apv[j] = ap;  // alpha~_{t-1}, read by every thread below
