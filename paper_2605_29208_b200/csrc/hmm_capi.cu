@@ -377,22 +377,30 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
                             : dispatch_fb_small<float>(K, a, cfg, g.global, grid, block, g.smem, st);
   } else {
     const int threads = 32 * ((K + 31) / 32);
-    // A (padded pitch K + 1), vector, reduction scratch, xi accumulators, alpha~_{t-1}
-    const size_t smem = (size_t)(K * (K + 1) + K + 32 + K * K + K) * esz;
+    // vector + alpha~_{t-1} (padded to KM) and the reduction scratch; A and
+    // the xi accumulators live in registers
+    const int KM = K <= 16 ? 16 : K <= 32 ? 32 : 64;
+    const bool xreg = esz * KM <= 256;
+    const size_t smem = (size_t)(2 * KM + 128 + (xreg ? 0 : KM * 64)) * esz;
     // log b for the whole batch first (fully parallel), then the sweeps
     void* lbw = (char*)workspace + align256((size_t)N * K * esz);
     const int64_t eblocks = std::min<int64_t>((N + 255) / 256, 148 * 16);
+#define LHMM_FBL(RR, KMV)                                                                        \
+  fb_large_kernel<RR, KMV><<<(unsigned)B, threads, smem, st>>>(a, K, (const RR*)lbw)
     if (dtype == LOGHMM_F64) {
       emission_kernel<double><<<(unsigned)eblocks, 256, 0, st>>>(
           model, (const double*)y0, (const double*)a.y1, N, K, lgamma_lut, lut_n, (double*)lbw);
-      cudaFuncSetAttribute(fb_large_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fb_large_kernel<double><<<(unsigned)B, threads, smem, st>>>(a, K, (const double*)lbw);
+      if (KM == 16) LHMM_FBL(double, 16);
+      else if (KM == 32) LHMM_FBL(double, 32);
+      else LHMM_FBL(double, 64);
     } else {
       emission_kernel<float><<<(unsigned)eblocks, 256, 0, st>>>(
           model, (const float*)y0, (const float*)a.y1, N, K, lgamma_lut, lut_n, (float*)lbw);
-      cudaFuncSetAttribute(fb_large_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      fb_large_kernel<float><<<(unsigned)B, threads, smem, st>>>(a, K, (const float*)lbw);
+      if (KM == 16) LHMM_FBL(float, 16);
+      else if (KM == 32) LHMM_FBL(float, 32);
+      else LHMM_FBL(float, 64);
     }
+#undef LHMM_FBL
     e = cudaGetLastError();
   }
   return e == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;

@@ -39,6 +39,38 @@ __device__ __forceinline__ R block_sum(R v, R* red, int nw) {
   return m;
 }
 
+// Double-buffered block reductions of one or two values: one barrier each
+// (reduction k+2 reuses reduction k's buffer only after every thread has
+// passed reduction k+1's barrier, i.e. finished reading reduction k).
+template <typename R>
+struct BRed {
+  R* red;  // 4 * 32 elements
+  int nw;
+  int buf;
+  __device__ __forceinline__ BRed(R* r, int n) : red(r), nw(n), buf(0) {}
+  // (max a, op b) where op = max (kMax) or sum
+  template <bool kSecondMax>
+  __device__ __forceinline__ void two(R& a, R& b) {
+    a = warp_max(a);
+    b = kSecondMax ? warp_max(b) : warp_sum(b);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    R* rb = red + buf * 64;
+    if (lane == 0) {
+      rb[w] = a;
+      rb[32 + w] = b;
+    }
+    __syncthreads();
+    R x = rb[0], y = rb[32];
+    for (int i = 1; i < nw; ++i) {
+      x = fmax(x, rb[i]);
+      y = kSecondMax ? fmax(y, rb[32 + i]) : y + rb[32 + i];
+    }
+    a = x;
+    b = y;
+    buf ^= 1;
+  }
+};
+
 // Observation features needed by the E-step statistics only (no lgamma LUT).
 template <typename R>
 __device__ __forceinline__ void stat_features(ObsFeat<R>& f, R y, int fam) {
@@ -51,17 +83,45 @@ __device__ __forceinline__ void stat_features(ObsFeat<R>& f, R y, int fam) {
 // blockDim.x = 32 * ceil(K/32); thread j < K owns state j.  The emission
 // log-densities come precomputed ([N, K], emission_kernel) and every per-step
 // load (log b, y, alpha~) is issued one step ahead, off the recursion chain.
-template <typename R>
+// Dot product of a register array with a shared-memory vector (read 16 bytes
+// at a time; entries >= K of the vector are zero).
+template <typename R, int KM>
+__device__ __forceinline__ R reg_dot(const R (&r)[KM], const R* __restrict__ v) {
+  R c[4] = {R(0), R(0), R(0), R(0)};
+  if constexpr (sizeof(R) == 4) {
+#pragma unroll
+    for (int i = 0; i < KM; i += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(v + i);
+      c[0] = fma(r[i], q.x, c[0]);
+      c[1] = fma(r[i + 1], q.y, c[1]);
+      c[2] = fma(r[i + 2], q.z, c[2]);
+      c[3] = fma(r[i + 3], q.w, c[3]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < KM; i += 2) {
+      const double2 q = *reinterpret_cast<const double2*>(v + i);
+      c[(i >> 1) & 3] = fma(r[i], q.x, c[(i >> 1) & 3]);
+      c[((i >> 1) + 2) & 3] = fma(r[i + 1], q.y, c[((i >> 1) + 2) & 3]);
+    }
+  }
+  return (c[0] + c[1]) + (c[2] + c[3]);
+}
+
+// KM: padded state count (16, 32 or 64).  Thread j keeps column j of A
+// (forward), row j of A (backward) and column j of the xi accumulators in
+// registers; only the carried vectors go through shared memory.
+template <typename R, int KM>
 __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, const R* __restrict__ lbws) {
   typedef Num<R> N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // A with a padded row pitch (K + 1): row reads A[j][.] across threads j
-  // and column reads A[.][j] are both bank-conflict free
-  const int AP = K + 1;
-  R* As = reinterpret_cast<R*>(smem_raw);  // K * AP
-  R* av = As + K * AP;                     // K (current vector)
-  R* red = av + K;                         // 32
-  R* apv = red + 32 + K * K;               // K (alpha~_{t-1}, backward sweep)
+  // xi accumulators in registers when they fit (fp32, or fp64 with KM <= 32),
+  // else a [KM][64] shared array (column j owned by thread j)
+  constexpr bool XREG = (int)sizeof(R) * KM <= 256;
+  R* av = reinterpret_cast<R*>(smem_raw);  // KM (current vector, zero padded)
+  R* red = av + KM;                         // 128 (double-buffered reductions)
+  R* apv = red + 128;                       // KM (alpha~_{t-1}, backward sweep)
+  R* Xs = apv + KM;                         // [KM][64] when !XREG
   const int tid = threadIdx.x;
   const int nw = blockDim.x >> 5;
   const int64_t b = blockIdx.x;
@@ -71,7 +131,13 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   const bool act = tid < K;
   const int j = act ? tid : 0;
   const loghmm_model_t* md = a.model;
-  for (int e = tid; e < K * K; e += blockDim.x) As[(e / K) * AP + e % K] = (R)md->A[e];
+  R Acol[KM];  // column j of A (forward sweep only)
+#pragma unroll
+  for (int i = 0; i < KM; ++i) Acol[i] = (act && i < K) ? (R)md->A[i * K + j] : R(0);
+  if (tid < KM) {
+    av[tid] = R(0);
+    apv[tid] = R(0);
+  }
   const EmP<R> p0 = load_emission<R>(md->em[0][j]);
   EmP<R> p1;
   const bool two = a.n_streams > 1;
@@ -89,7 +155,8 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   int dead_t = INT_MAX;
   __syncthreads();
 
-  // forward
+  // forward (two barriers per step)
+  BRed<R> br(red, nw);
   double lam = 0.0;
   R a_j = R(0);
   const R* __restrict__ lbs = lbws + start * K;
@@ -108,19 +175,13 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
     if (t == 0) {
       u = lpi + lb;
     } else {
-      R c4[4] = {R(0), R(0), R(0), R(0)};  // four independent chains
-      int i = 0;
-      for (; i + 3 < K; i += 4)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) c4[q] = fma(av[i + q], As[(i + q) * AP + j], c4[q]);
-      for (; i < K; ++i) c4[0] = fma(av[i], As[i * AP + j], c4[0]);
-      const R acc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+      const R acc = reg_dot<R, KM>(Acol, av);
       u = (acc > R(0) ? N::flog(acc) : N::ninf()) + lb;
     }
     if (act && outA) outA[(int64_t)t * K + j] = (R)lam + u;
-    const R mlb = block_max(act ? lb : N::ninf(), red, nw);
+    R M = act ? u : N::ninf(), mlb = act ? lb : N::ninf();
+    br.two<true>(M, mlb);
     if (!(mlb > N::ninf()) && t < dead_t) dead_t = t;
-    const R M = block_max(act ? u : N::ninf(), red, nw);
     a_j = (M > N::ninf()) ? N::fexp(u - M) : R(0);
     if (M > N::ninf()) lam += (double)M;
     if (act) {
@@ -141,9 +202,14 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   R st[2][LOGHMM_NSLOT];
   for (int s = 0; s < 2; ++s)
     for (int q = 0; q < LOGHMM_NSLOT; ++q) st[s][q] = R(0);
-  R* X = red + 32;  // K*K xi accumulators (column j owned by thread j)
-  for (int i = 0; i < K; ++i)
-    if (act) X[i * K + j] = R(0);
+  R Arow[KM];  // row j of A (backward sweep)
+#pragma unroll
+  for (int i = 0; i < KM; ++i) Arow[i] = (act && i < K) ? (R)md->A[j * K + i] : R(0);
+  R Xc[XREG ? KM : 1];
+#pragma unroll
+  for (int i = 0; i < (XREG ? KM : 1); ++i) Xc[i] = R(0);
+  if (!XREG)
+    for (int i = 0; i < KM; ++i) Xs[i * 64 + tid] = R(0);
   R r = R(0);  // log beta~ at current t (max 0)
   double rho = 0.0;
   R bl = (act && T > 0) ? lbs[(int64_t)(T - 1) * K + j] : N::ninf();
@@ -160,9 +226,11 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
     ObsFeat<R> f0, f1;
     stat_features<R>(f0, v0, p0.fam);
     if (two) stat_features<R>(f1, v1, p1.fam);
-    // gamma at t: a_t * exp(r)
+    // gamma at t: a_t * exp(r); with it the max of u = lb_t + r for the step
+    // to t-1 (one reduction for both)
     const R q = act ? N::fexp(r) : R(0);
-    const R gz = block_sum(at * q, red, nw);
+    R M = act ? lb + r : N::ninf(), gz = at * q;
+    br.two<false>(M, gz);
     const R gj = at * q / gz;
     if (act) {
       if (outB) outB[(int64_t)t * K + j] = (R)rho + r;
@@ -182,7 +250,6 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
     if (t == 0) break;
     // step to t-1: u = lb_t + r; w = exp(u - M); q_{t-1} = A w
     const R u = act ? lb + r : N::ninf();
-    const R M = block_max(u, red, nw);
     const bool fin = M > N::ninf();
     const R w = (act && fin) ? N::fexp(u - M) : R(0);
     const R ap = bat;  // alpha~_{t-1}, prefetched above
@@ -191,35 +258,46 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
       apv[j] = ap;  // alpha~_{t-1}, read by every thread below
     }
     __syncthreads();
-    R acc = R(0);
-    if (act) {
-      R c4[4] = {R(0), R(0), R(0), R(0)};
-      int jj = 0;
-      for (; jj + 3 < K; jj += 4)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) c4[q] = fma(As[j * AP + jj + q], wv[jj + q], c4[q]);
-      for (; jj < K; ++jj) c4[0] = fma(As[j * AP + jj], wv[jj], c4[0]);
-      acc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
-    }
-    // xi_{t-1}(i, j) = a_{t-1}[i] A_ij w_j / Z, Z = sum_i a_{t-1}[i] q_i
-    const R Z = block_sum(ap * acc, red, nw);
+    const R acc = act ? reg_dot<R, KM>(Arow, wv) : R(0);
+    // xi_{t-1}(i, j) = a_{t-1}[i] A_ij w_j / Z, Z = sum_i a_{t-1}[i] q_i;
+    // with it the max of log q for the renormalisation (one reduction)
+    const R lq = acc > R(0) ? N::flog(acc) : N::ninf();
+    R mq = act ? lq : N::ninf(), Z = ap * acc;
+    br.two<false>(mq, Z);
     const R iz = R(1) / Z;
     // thread j (as column) accumulates X[i][j] += a_i/Z * w_j
     if (act) {
       const R wz = w * iz;
-      for (int i = 0; i < K; ++i) {
-        X[i * K + j] = fma(apv[i], wz, X[i * K + j]);
-        if (outX) outX[((int64_t)(t - 1) * K + i) * K + j] = apv[i] * iz * As[i * AP + j] * w;
+      if constexpr (XREG && sizeof(R) == 4) {
+#pragma unroll
+        for (int i = 0; i < KM; i += 4) {
+          const float4 q = *reinterpret_cast<const float4*>(apv + i);
+          Xc[i] = fma(q.x, wz, Xc[i]);
+          Xc[i + 1] = fma(q.y, wz, Xc[i + 1]);
+          Xc[i + 2] = fma(q.z, wz, Xc[i + 2]);
+          Xc[i + 3] = fma(q.w, wz, Xc[i + 3]);
+        }
+      } else if constexpr (XREG) {
+#pragma unroll
+        for (int i = 0; i < KM; i += 2) {
+          const double2 q = *reinterpret_cast<const double2*>(apv + i);
+          Xc[i] = fma(q.x, wz, Xc[i]);
+          Xc[i + 1] = fma(q.y, wz, Xc[i + 1]);
+        }
+      } else {
+        for (int i = 0; i < K; ++i) Xs[i * 64 + tid] = fma(apv[i], wz, Xs[i * 64 + tid]);
       }
+      if (outX)
+        for (int i = 0; i < K; ++i)
+          outX[((int64_t)(t - 1) * K + i) * K + j] = apv[i] * iz * (R)md->A[i * K + j] * w;
     }
-    const R lq = acc > R(0) ? N::flog(acc) : N::ninf();
-    const R mq = block_max(act ? lq : N::ninf(), red, nw);
     if (mq > N::ninf()) {
       r = lq - mq;
       rho += (fin ? (double)M : 0.0) + (double)mq;
     }
     // note: log_beta[t-1] = rho_prev + M + lq  ==  (rho + r) after the update
-    __syncthreads();
+    // (no end-of-step barrier: the next step's first reduction orders this
+    // step's wv / apv reads before its writes)
   }
   __syncthreads();
   const int tid0 = tid;
@@ -227,7 +305,13 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   if (a.partials) {
     double* row = a.partials + b * a.stats_width;
     if (act) {
-      for (int i = 0; i < K; ++i) row[i * K + j] = (double)X[i * K + j] * (double)As[i * AP + j];
+      if constexpr (XREG) {
+#pragma unroll
+        for (int i = 0; i < KM; ++i)
+          if (i < K) row[i * K + j] = (double)Xc[i] * md->A[i * K + j];
+      } else {
+        for (int i = 0; i < K; ++i) row[i * K + j] = (double)Xs[i * 64 + tid] * md->A[i * K + j];
+      }
       row[K * K + j] = (double)gtot;
       row[K * K + K + j] = (double)g0;
       for (int s = 0; s < 2; ++s)

@@ -559,3 +559,41 @@ def test_pipeline_host_slices_match_device_run(dtype):
         assert torch.equal(p.dm_next.buf, ref_model), slices
         assert torch.equal(p.vit.path, ref_path), slices
         assert torch.equal(p.fb.gamma, ref_gamma), slices
+
+
+@pytest.mark.parametrize("K", [9, 20, 40, 64])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_large_k_posteriors_xi_and_viterbi(K, dtype):
+    """K > 8 (one CTA per sequence, A and the xi accumulators in registers or
+    shared memory by size): LL, gamma, log alpha/beta, per-step xi and the
+    E-step statistics against the oracle on ragged sequences; Viterbi
+    bit-exact."""
+    rng = np.random.default_rng(500 + K)
+    pi = rng.dirichlet(np.ones(K))
+    A = rng.dirichlet(np.ones(K), size=K) * 0.5 + 0.5 * np.eye(K)
+    A /= A.sum(1, keepdims=True)
+    m = H.HmmModel(pi, A, tuple(H.Poisson(float(r)) for r in np.linspace(0.5, 12.0, K)))
+    seqs = [rng.poisson(5.0, n).astype(float) for n in (3, 50, 257)]
+    r = H.posteriors_batch(m, seqs, dtype=dtype, include_xi=True)
+    lp, la = O.model_tables(pi, A)
+    tol = 1e-9 if dtype == "float64" else 1e-5
+    X_ = r.xi.cpu().numpy().astype(np.float64)
+    for b, y in enumerate(seqs):
+        o = O.posteriors(lp, la, O.emission_matrix(to_tuples(m), y), include_xi=True)
+        s = slice(r.offsets[b], r.offsets[b + 1])
+        xs = slice(r.offsets[b] - b, r.offsets[b + 1] - b - 1)
+        assert r.log_likelihood[b].item() == pytest.approx(o["ll"], rel=1e-9 if dtype == "float64" else 1e-4)
+        np.testing.assert_allclose(r.gamma[s].double().cpu().numpy(), o["gamma"], atol=tol)
+        np.testing.assert_allclose(X_[xs], o["xi"], atol=tol)
+    vit = H.viterbi_batch(m, seqs, back=True)
+    for b, y in enumerate(seqs):
+        p, j, bk = O.viterbi(lp, la, O.emission_matrix(to_tuples(m), y))
+        s = slice(vit.offsets[b], vit.offsets[b + 1])
+        assert np.array_equal(vit.path[s].cpu().numpy(), p)
+        assert np.array_equal(vit.back[s].cpu().numpy().astype(np.int64), bk)
+        assert vit.log_joint[b].item() == j
+    # E-step statistics (xi totals, gamma totals, Poisson sums) through the fit
+    fitted, rep = H.baum_welch(m, seqs, H.TrainingConfig(max_iterations=2, rel_tol=1e-300))
+    pi2, A2, em2, trace, _, _ = O.baum_welch(pi, A, to_tuples(m), seqs, 2)
+    np.testing.assert_allclose(rep.log_likelihood_trace, trace, rtol=1e-9)
+    np.testing.assert_allclose(fitted.transitions, A2, atol=1e-9)
