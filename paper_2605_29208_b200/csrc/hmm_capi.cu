@@ -494,8 +494,14 @@ int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64
     return LOGHMM_EINVAL;
   // the widest statistics vector (K = LOGHMM_MAX_STATES) fits the default
   // 48 KB dynamic shared-memory window
+  // + the transition scratch (K*K + K + 1 doubles), sized for K = 64
   const int64_t wmax = (int64_t)loghmm_stats_width(LOGHMM_MAX_STATES, 2) + 1;
-  mstep_kernel<<<1, 256, (size_t)wmax * sizeof(double), (cudaStream_t)stream>>>(
+  const size_t msm = (size_t)(wmax + LOGHMM_MAX_STATES * LOGHMM_MAX_STATES + LOGHMM_MAX_STATES + 1) *
+                     sizeof(double);
+  if (cudaFuncSetAttribute(mstep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm) !=
+      cudaSuccess)
+    return LOGHMM_ELAUNCH;
+  mstep_kernel<<<1, 256, msm, (cudaStream_t)stream>>>(
       model_in, totals, wmax, n_sequences, collapse_epsilon, nu_ceiling, nu_tol, max_newton,
       model_out, status, guard_state, var_ratio);
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
@@ -527,7 +533,11 @@ int32_t loghmm_reduce_mstep(const double* partials, const double* ll, int64_t B,
   // that both reduction levels keep ~B / (G * sqrt(B)) rows per thread (one
   // batch of independent loads each)
   constexpr int kRedThreads = 1024;
-  const size_t smem = (size_t)(width + 1 + kRedThreads) * sizeof(double);
+  // (+ the M-step's transition scratch, K*K + K + 1 doubles; K from the
+  // statistics width K^2 + 2K + 2K*NSLOT)
+  int64_t Ks = 1;
+  while (Ks < LOGHMM_MAX_STATES && Ks * Ks + 2 * Ks + 2 * Ks * LOGHMM_NSLOT < width) ++Ks;
+  const size_t smem = (size_t)(width + 1 + kRedThreads + Ks * Ks + Ks + 1) * sizeof(double);
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(reduce_mstep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)

@@ -198,11 +198,13 @@ __global__ void __launch_bounds__(256) reduce_stats_kernel(const double* __restr
 //  [13]    n (total weight),  [14] sum w log y (gamma),  [15] old shape (gamma)
 constexpr int kGuardStride = 16;
 
+// Called by every thread of the block (it synchronises); `scratch` holds
+// K*K + K + 1 doubles of shared memory.
 __device__ void mstep_body(const loghmm_model_t* __restrict__ min_, const double* __restrict__ tot,
                            int64_t nseq, double eps, double nu_ceiling, double nu_tol,
                            int max_newton, loghmm_model_t* __restrict__ mout,
                            int32_t* __restrict__ status, double* __restrict__ guard,
-                           double var_ratio, int tid, int nthreads) {
+                           double var_ratio, int tid, int nthreads, double* __restrict__ scratch) {
   const int K = min_->K;
   const int S = min_->n_streams;
   const int width_xi = K * K;
@@ -215,28 +217,40 @@ __device__ void mstep_body(const loghmm_model_t* __restrict__ min_, const double
     mout->n_streams = S;
   }
   // ---- transitions and initial distribution (training.py:105-127) ----
-  if (tid < K) {
-    // row i: A[i, :] = xi[i, :] / gt[i], renormalised (no read-back of mout)
-    const int i = tid;
-    const double g = gt[i];
-    double total = 0.0;
-    if (g >= eps)
-      for (int j = 0; j < K; ++j) total += xi[i * K + j] / g;
-    const bool upd = g >= eps && total > 0.0;
-    for (int j = 0; j < K; ++j) {
-      const double v = upd ? (xi[i * K + j] / g) / total : min_->A[i * K + j];
-      mout->A[i * K + j] = v;
-      mout->log_A[i * K + j] = v > 0.0 ? log(v) : -CUDART_INF;
-    }
+  // Spread over (i, j): the per-entry divisions and logs run in parallel; the
+  // row totals and the pi normaliser are summed in the reference's order.
+  double* vb = scratch;             // [K*K] xi[i, j] / gamma_tot[i]
+  double* rowt = scratch + K * K;   // [K] row totals
+  double* pis = rowt + K;           // [1] sum_j g0[j] / nseq
+  for (int e = tid; e < K * K; e += nthreads) {
+    const double g = gt[e / K];
+    vb[e] = g >= eps ? xi[e] / g : 0.0;
   }
-  if (tid == 0) {
-    double pis = 0.0;
-    for (int j = 0; j < K; ++j) pis += g0[j] / (double)nseq;
-    for (int j = 0; j < K; ++j) {
-      const double p = (g0[j] / (double)nseq) / pis;
-      mout->pi[j] = p;
-      mout->log_pi[j] = p > 0.0 ? log(p) : -CUDART_INF;
-    }
+  __syncthreads();
+  for (int i = tid; i < K; i += nthreads) {
+    double total = 0.0;
+    if (gt[i] >= eps)
+      for (int j = 0; j < K; ++j) total += vb[i * K + j];
+    rowt[i] = total;
+  }
+  if (tid == nthreads - 1) {
+    double p = 0.0;
+    for (int j = 0; j < K; ++j) p += g0[j] / (double)nseq;
+    pis[0] = p;
+  }
+  __syncthreads();
+  for (int e = tid; e < K * K; e += nthreads) {
+    const int i = e / K;
+    const double total = rowt[i];
+    const bool upd = gt[i] >= eps && total > 0.0;
+    const double v = upd ? vb[e] / total : min_->A[e];
+    mout->A[e] = v;
+    mout->log_A[e] = v > 0.0 ? log(v) : -CUDART_INF;
+  }
+  for (int j = tid; j < K; j += nthreads) {
+    const double p = (g0[j] / (double)nseq) / pis[0];
+    mout->pi[j] = p;
+    mout->log_pi[j] = p > 0.0 ? log(p) : -CUDART_INF;
   }
   // ---- emissions (training.py:130-148 -> distributions.py:1094 refit) ----
   for (int idx = tid; idx < S * K; idx += nthreads) {
@@ -442,7 +456,7 @@ __global__ void __launch_bounds__(256) mstep_kernel(const loghmm_model_t* __rest
   for (int64_t c = threadIdx.x; c < w1; c += blockDim.x) tot_s[c] = tot[c];
   __syncthreads();
   mstep_body(min_, tot_s, nseq, eps, nu_ceiling, nu_tol, max_newton, mout, status, guard, var_ratio,
-             threadIdx.x, blockDim.x);
+             threadIdx.x, blockDim.x, tot_s + w1);
 }
 
 // Fused statistics reduction + M-step (single rank).  Block r sums rows
@@ -517,7 +531,7 @@ __global__ void __launch_bounds__(1024) reduce_mstep_kernel(
   __syncthreads();
   if (do_mstep)
     mstep_body(min_, tot_s, nseq, eps, nu_ceiling, nu_tol, max_newton, mout, status, guard,
-               var_ratio, threadIdx.x, blockDim.x);
+               var_ratio, threadIdx.x, blockDim.x, tot_s + W1 + blockDim.x);
 }
 
 // Guard pass: for every active Student-t state j (stream `sidx`), partial sums
