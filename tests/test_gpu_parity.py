@@ -597,3 +597,36 @@ def test_large_k_posteriors_xi_and_viterbi(K, dtype):
     pi2, A2, em2, trace, _, _ = O.baum_welch(pi, A, to_tuples(m), seqs, 2)
     np.testing.assert_allclose(rep.log_likelihood_trace, trace, rtol=1e-9)
     np.testing.assert_allclose(fitted.transitions, A2, atol=1e-9)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_error_semantics_equal_length_batches(dtype):
+    """Error paths of the equal-length decomposition (chunk operators + meet in
+    the middle for fp32): a dead observation, an unreachable path and NaN are
+    reported with the reference's exceptions, sequence and index."""
+    rng = np.random.default_rng(3)
+    m = H.HmmModel([0.5, 0.5], [[0.9, 0.1], [0.2, 0.8]], (H.Poisson(2.0), H.Poisson(5.0)))
+    data = rng.poisson(3.0, size=(4, 64)).astype(np.float64)
+    dead = data.copy()
+    dead[2, 37] = 0.5  # outside the support of every state
+    with pytest.raises(H.InfeasibleSequenceError, match="sequence impossible under model"):
+        H.posteriors_batch(m, dead, dtype=dtype)
+    with pytest.raises(H.TrainingError, match="sequence 2, index 37"):
+        H.baum_welch(m, [dead[b] for b in range(4)], H.TrainingConfig(max_iterations=2))
+    nan = data.copy()
+    nan[1, 50] = np.nan
+    with pytest.raises(ValueError, match="NaN"):
+        H.posteriors_batch(m, nan, dtype=dtype)
+    # impossible without a dead row: state 1 (Gaussian) is unreachable, and
+    # y <= 0 is outside the support of state 0 (Gamma) only
+    m2 = H.HmmModel([1.0, 0.0], [[1.0, 0.0], [0.0, 1.0]], (H.Gamma(2.0, 1.0), H.Gaussian(0.0, 1.0)))
+    ok = rng.gamma(2.0, 1.0, size=(4, 64))
+    bad = ok.copy()
+    bad[3, 10] = -1.0
+    r = H.posteriors_batch(m2, bad, dtype=dtype, check=False)
+    ll = r.log_likelihood.cpu().numpy()
+    assert np.isfinite(ll[:3]).all() and ll[3] == -np.inf
+    with pytest.raises(H.InfeasibleSequenceError, match="sequence impossible under model"):
+        H.posteriors_batch(m2, bad, dtype=dtype)
+    with pytest.raises(H.TrainingError, match="sequence 3 is impossible"):
+        H.baum_welch(m2, [bad[b] for b in range(4)], H.TrainingConfig(max_iterations=2))
