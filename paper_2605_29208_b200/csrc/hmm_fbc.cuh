@@ -315,21 +315,6 @@ struct Em2 {
   }
 };
 
-// Power-of-two renormalisation of a vector, exponent added to a log2 offset
-// kept in R (sums of small integers: exact).
-template <typename R, int K>
-__device__ __forceinline__ void renorm_vec(R (&v)[K], R& off) {
-  R m = v[0];
-#pragma unroll
-  for (int i = 1; i < K; ++i) m = rmax(m, v[i]);
-  if (m > R(0)) {
-    int e;
-    const R s = Num<R>::pow2_scale(m, e);
-    off += (R)e;
-#pragma unroll
-    for (int i = 0; i < K; ++i) v[i] *= s;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Tensor memory as per-warp scratch for the parked vectors (fp32).  A CTA is
