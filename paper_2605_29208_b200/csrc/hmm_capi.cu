@@ -376,17 +376,25 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
     e = dtype == LOGHMM_F64 ? dispatch_fb_small<double>(K, a, cfg, g.global, grid, block, g.smem, st)
                             : dispatch_fb_small<float>(K, a, cfg, g.global, grid, block, g.smem, st);
   } else {
-    const int threads = 32 * ((K + 31) / 32);
-    // vector + alpha~_{t-1} (padded to KM) and the reduction scratch; A and
-    // the xi accumulators live in registers
+    // four lanes per state; vector + alpha~_{t-1} (padded to KM) and the
+    // reduction scratch in shared memory, A and the xi accumulators in registers
     const int KM = K <= 16 ? 16 : K <= 32 ? 32 : 64;
-    const bool xreg = esz * KM <= 256;
-    const size_t smem = (size_t)(2 * KM + 128 + (xreg ? 0 : KM * 64)) * esz;
+    // lanes per state: 1 measured fastest at K = 64 (the per-step block
+    // reductions cost more with more warps than the split dot products save);
+    // 2 and 4 stay selectable for A/B runs
+    int lps = 1;
+    if (const char* env = getenv("LOGHMM_FBL_LPS")) lps = atoi(env) >= 4 ? 4 : atoi(env) >= 2 ? 2 : 1;
+    const int threads = std::max(32, lps * KM);
+    const size_t smem = (size_t)(2 * KM + 128 + kRing * 4 * KM) * esz;
     // log b for the whole batch first (fully parallel), then the sweeps
     void* lbw = (char*)workspace + align256((size_t)N * K * esz);
     const int64_t eblocks = std::min<int64_t>((N + 255) / 256, 148 * 16);
 #define LHMM_FBL(RR, KMV)                                                                        \
-  fb_large_kernel<RR, KMV><<<(unsigned)B, threads, smem, st>>>(a, K, (const RR*)lbw)
+  do {                                                                                           \
+    if (lps == 4) fb_large_kernel<RR, KMV, 4><<<(unsigned)B, threads, smem, st>>>(a, K, (const RR*)lbw); \
+    else if (lps == 2) fb_large_kernel<RR, KMV, 2><<<(unsigned)B, threads, smem, st>>>(a, K, (const RR*)lbw); \
+    else fb_large_kernel<RR, KMV, 1><<<(unsigned)B, threads, smem, st>>>(a, K, (const RR*)lbw); \
+  } while (0)
     if (dtype == LOGHMM_F64) {
       emission_kernel<double><<<(unsigned)eblocks, 256, 0, st>>>(
           model, (const double*)y0, (const double*)a.y1, N, K, lgamma_lut, lut_n, (double*)lbw);
@@ -458,15 +466,21 @@ int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm
                             : dispatch_vit_small<float>(K, a, cfg, g.global, grid, block, g.smem, st);
   } else {
     const int esz = dtype == LOGHMM_F64 ? 8 : 4;
-    const int threads = 32 * ((K + 31) / 32);
-    const size_t smem = (size_t)(K * K + K) * esz + 256 * (size_t)K;
+    const int KM = K <= 16 ? 16 : K <= 32 ? 32 : 64;
+    const int threads = 4 * KM;  // four lanes per destination state
+    const size_t smem = (size_t)(2 * KM) * esz + 256 * (size_t)K;
+#define LHMM_VL(RR, KMV)                                                                         \
+  viterbi_large_kernel<RR, KMV><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace)
     if (dtype == LOGHMM_F64) {
-      cudaFuncSetAttribute(viterbi_large_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      viterbi_large_kernel<double><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace);
+      if (KM == 16) LHMM_VL(double, 16);
+      else if (KM == 32) LHMM_VL(double, 32);
+      else LHMM_VL(double, 64);
     } else {
-      cudaFuncSetAttribute(viterbi_large_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      viterbi_large_kernel<float><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace);
+      if (KM == 16) LHMM_VL(float, 16);
+      else if (KM == 32) LHMM_VL(float, 32);
+      else LHMM_VL(float, 64);
     }
+#undef LHMM_VL
     e = cudaGetLastError();
   }
   return e == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;

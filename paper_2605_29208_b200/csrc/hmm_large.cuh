@@ -80,60 +80,83 @@ __device__ __forceinline__ void stat_features(ObsFeat<R>& f, R y, int fam) {
   if (fam == LOGHMM_FAM_POISSON) f.pois_ok = (y >= R(0)) && (floor(y) == y);
 }
 
-// blockDim.x = 32 * ceil(K/32); thread j < K owns state j.  The emission
-// log-densities come precomputed ([N, K], emission_kernel) and every per-step
-// load (log b, y, alpha~) is issued one step ahead, off the recursion chain.
-// Dot product of a register array with a shared-memory vector (read 16 bytes
-// at a time; entries >= K of the vector are zero).
-template <typename R, int KM>
-__device__ __forceinline__ R reg_dot(const R (&r)[KM], const R* __restrict__ v) {
-  R c[4] = {R(0), R(0), R(0), R(0)};
-  if constexpr (sizeof(R) == 4) {
-#pragma unroll
-    for (int i = 0; i < KM; i += 4) {
-      const float4 q = *reinterpret_cast<const float4*>(v + i);
-      c[0] = fma(r[i], q.x, c[0]);
-      c[1] = fma(r[i + 1], q.y, c[1]);
-      c[2] = fma(r[i + 2], q.z, c[2]);
-      c[3] = fma(r[i + 3], q.w, c[3]);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < KM; i += 2) {
-      const double2 q = *reinterpret_cast<const double2*>(v + i);
-      c[(i >> 1) & 3] = fma(r[i], q.x, c[(i >> 1) & 3]);
-      c[((i >> 1) + 2) & 3] = fma(r[i + 1], q.y, c[((i >> 1) + 2) & 3]);
-    }
+// Quarter-split layout: four adjacent lanes (j, q), q = tid & 3, share state
+// j = tid >> 2.  Lane q holds the 16-byte chunks c = q, q + 4, ... of column
+// j of A (forward), row j of A (backward) and column j of the xi
+// accumulators, so a K-long dot product is K/4 FMAs per lane plus two xor
+// shuffles (bit-identical in all four lanes), and the interleaved chunks keep
+// the shared-memory vector reads conflict-free.
+template <typename R, int KM, int P = 4>
+struct Quarter {
+  static constexpr int EPC = 16 / (int)sizeof(R);  // elements per 16-byte chunk
+  static constexpr int NQC = KM / EPC / P;         // chunks per lane
+  static constexpr int NQ = NQC * EPC;             // elements per lane (KM / P)
+  static __device__ __forceinline__ int idx(int q, int s) {
+    return (P * (s / EPC) + q) * EPC + s % EPC;
   }
-  return (c[0] + c[1]) + (c[2] + c[3]);
-}
+  // sum_i r[i] v[i] over the lane's elements, then over the four lanes
+  static __device__ __forceinline__ R dot(const R (&r)[NQ], const R* __restrict__ v, int q) {
+    R c[2] = {R(0), R(0)};
+    if constexpr (sizeof(R) == 4) {
+#pragma unroll
+      for (int m = 0; m < NQC; ++m) {
+        const float4 x = *reinterpret_cast<const float4*>(v + (P * m + q) * 4);
+        c[0] = fma(r[4 * m], x.x, c[0]);
+        c[1] = fma(r[4 * m + 1], x.y, c[1]);
+        c[0] = fma(r[4 * m + 2], x.z, c[0]);
+        c[1] = fma(r[4 * m + 3], x.w, c[1]);
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < NQC; ++m) {
+        const double2 x = *reinterpret_cast<const double2*>(v + (P * m + q) * 2);
+        c[0] = fma(r[2 * m], x.x, c[0]);
+        c[1] = fma(r[2 * m + 1], x.y, c[1]);
+      }
+    }
+    R p = c[0] + c[1];
+#pragma unroll
+    for (int o = 1; o < P; o <<= 1) p += __shfl_xor_sync(kFull, p, o);
+    return p;
+  }
+};
 
-// KM: padded state count (16, 32 or 64).  Thread j keeps column j of A
-// (forward), row j of A (backward) and column j of the xi accumulators in
-// registers; only the carried vectors go through shared memory.
-template <typename R, int KM>
-__global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, const R* __restrict__ lbws) {
+// blockDim.x = 4 * KM (KM: padded state count, 16, 32 or 64), four lanes per
+// state (Quarter).  The emission log-densities come precomputed ([N, K],
+// emission_kernel) and every per-step load (log b, y, alpha~) is issued one
+// step ahead, off the recursion chain.  Lane q == 0 of each state does the
+// per-state work (outputs, statistics); only the carried vectors go through
+// shared memory.
+constexpr int kRing = 16;  // fb_large_kernel input ring depth (steps)
+
+template <typename R, int KM, int P>
+__global__ void __launch_bounds__(256) fb_large_kernel(const FBArgs a, int K, const R* __restrict__ lbws) {
   typedef Num<R> N;
+  typedef Quarter<R, KM, P> Q;
+  constexpr int NQ = Q::NQ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // xi accumulators in registers when they fit (fp32, or fp64 with KM <= 32),
-  // else a [KM][64] shared array (column j owned by thread j)
-  constexpr bool XREG = (int)sizeof(R) * KM <= 256;
   R* av = reinterpret_cast<R*>(smem_raw);  // KM (current vector, zero padded)
   R* red = av + KM;                         // 128 (double-buffered reductions)
   R* apv = red + 128;                       // KM (alpha~_{t-1}, backward sweep)
-  R* Xs = apv + KM;                         // [KM][64] when !XREG
+  R* ring = apv + KM;                       // [kRing][4][KM] per-step inputs
   const int tid = threadIdx.x;
   const int nw = blockDim.x >> 5;
+  const int q = tid & (P - 1);
+  const int jt = tid / P;
   const int64_t b = blockIdx.x;
   if (b >= a.B) return;
   const int64_t start = a.offsets[b];
   const int T = (int)(a.offsets[b + 1] - start);
-  const bool act = tid < K;
-  const int j = act ? tid : 0;
+  const bool act = jt < K;
+  const bool lead = act && q == 0;
+  const int j = act ? jt : 0;
   const loghmm_model_t* md = a.model;
-  R Acol[KM];  // column j of A (forward sweep only)
+  R Acol[NQ];  // column j of A, this lane's elements (forward sweep only)
 #pragma unroll
-  for (int i = 0; i < KM; ++i) Acol[i] = (act && i < K) ? (R)md->A[i * K + j] : R(0);
+  for (int s = 0; s < NQ; ++s) {
+    const int i = Q::idx(q, s);
+    Acol[s] = (act && i < K) ? (R)md->A[i * K + j] : R(0);
+  }
   if (tid < KM) {
     av[tid] = R(0);
     apv[tid] = R(0);
@@ -160,39 +183,54 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   double lam = 0.0;
   R a_j = R(0);
   const R* __restrict__ lbs = lbws + start * K;
-  R lbn = (act && T > 0) ? lbs[j] : N::ninf();
-  R yn0 = T > 0 ? y0g[0] : R(0), yn1 = (two && T > 0) ? y1g[0] : R(0);
-  for (int t = 0; t < T; ++t) {
-    const R v0 = yn0, v1 = yn1;
-    const R lb = lbn;
-    if (t + 1 < T) {  // prefetch step t + 1
-      lbn = act ? lbs[(int64_t)(t + 1) * K + j] : N::ninf();
-      yn0 = y0g[t + 1];
-      if (two) yn1 = y1g[t + 1];
+  // Per-step inputs of state j (log b, y, alpha~) reach lane (j, 0) through a
+  // private shared-memory ring [kRing][4][KM] filled by cp.async kRing - 1
+  // steps ahead, so the global-load latency stays off the recursion chain.
+  // step t into ring position pos (forward pos = t, backward pos = T - 1 - t)
+  auto issue = [&](int t, int pos, bool with_alpha) {
+    if (lead) {
+      const bool ok = t >= 0 && t < T;
+      const int tc = ok ? t : 0;
+      R* sl = ring + (size_t)(pos % kRing) * 4 * KM;
+      cp_async<sizeof(R)>(sl + j, lbs + (int64_t)tc * K + j, ok);
+      cp_async<sizeof(R)>(sl + KM + j, y0g + tc, ok);
+      if (two) cp_async<sizeof(R)>(sl + 2 * KM + j, y1g + tc, ok);
+      if (with_alpha) cp_async<sizeof(R)>(sl + 3 * KM + j, aws + (int64_t)tc * K + j, ok);
     }
-    if (isnan(v0) || isnan(v1)) nan_seen = true;
+    cp_async_commit();
+  };
+  auto slot = [&](int t) -> const R* { return ring + (size_t)(t % kRing) * 4 * KM; };
+#pragma unroll 1
+  for (int d = 0; d < kRing - 1; ++d) issue(d, d, false);
+  for (int t = 0; t < T; ++t) {
+    issue(t + kRing - 1, t + kRing - 1, false);
+    cp_async_wait<kRing - 1>();
+    const R* sl = slot(t);
+    const R lb = lead ? sl[j] : N::ninf();
+    if (lead && (isnan(sl[KM + j]) || (two && isnan(sl[2 * KM + j])))) nan_seen = true;
     R u;
     if (t == 0) {
       u = lpi + lb;
     } else {
-      const R acc = reg_dot<R, KM>(Acol, av);
+      const R acc = Q::dot(Acol, av, q);
       u = (acc > R(0) ? N::flog(acc) : N::ninf()) + lb;
     }
-    if (act && outA) outA[(int64_t)t * K + j] = (R)lam + u;
-    R M = act ? u : N::ninf(), mlb = act ? lb : N::ninf();
+    if (lead && outA) outA[(int64_t)t * K + j] = (R)lam + u;
+    R M = lead ? u : N::ninf(), mlb = lb;
     br.two<true>(M, mlb);
     if (!(mlb > N::ninf()) && t < dead_t) dead_t = t;
     a_j = (M > N::ninf()) ? N::fexp(u - M) : R(0);
     if (M > N::ninf()) lam += (double)M;
-    if (act) {
+    if (lead) {
       av[j] = a_j;
       aws[(int64_t)t * K + j] = a_j;
     }
     __syncthreads();
   }
+  cp_async_wait_all();
   double LL;
   {
-    const R s = block_sum(act ? a_j : R(0), red, nw);
+    const R s = block_sum(lead ? a_j : R(0), red, nw);
     LL = s > R(0) ? lam + (double)N::flog(s) : -CUDART_INF;
   }
 
@@ -201,38 +239,41 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   R gtot = R(0), g0 = R(0);
   R st[2][LOGHMM_NSLOT];
   for (int s = 0; s < 2; ++s)
-    for (int q = 0; q < LOGHMM_NSLOT; ++q) st[s][q] = R(0);
-  R Arow[KM];  // row j of A (backward sweep)
+    for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][qq] = R(0);
+  R Arow[NQ];  // row j of A, this lane's elements (backward sweep)
 #pragma unroll
-  for (int i = 0; i < KM; ++i) Arow[i] = (act && i < K) ? (R)md->A[j * K + i] : R(0);
-  R Xc[XREG ? KM : 1];
+  for (int s = 0; s < NQ; ++s) {
+    const int i = Q::idx(q, s);
+    Arow[s] = (act && i < K) ? (R)md->A[j * K + i] : R(0);
+  }
+  R Xc[NQ];  // xi accumulators X[i][j], this lane's i
 #pragma unroll
-  for (int i = 0; i < (XREG ? KM : 1); ++i) Xc[i] = R(0);
-  if (!XREG)
-    for (int i = 0; i < KM; ++i) Xs[i * 64 + tid] = R(0);
+  for (int s = 0; s < NQ; ++s) Xc[s] = R(0);
   R r = R(0);  // log beta~ at current t (max 0)
   double rho = 0.0;
-  R bl = (act && T > 0) ? lbs[(int64_t)(T - 1) * K + j] : N::ninf();
-  R by0 = T > 0 ? y0g[T - 1] : R(0), by1 = (two && T > 0) ? y1g[T - 1] : R(0);
-  R bat = (act && T > 0) ? aws[(int64_t)(T - 1) * K + j] : R(0);
+  // ring position p = T - 1 - t (the sweep runs down)
+#pragma unroll 1
+  for (int d = 0; d < kRing - 1; ++d) issue(T - 1 - d, d, true);
   for (int t = T - 1; t >= 0; --t) {
-    const R v0 = by0, v1 = by1, lb = bl, at = bat;
-    if (t >= 1) {  // prefetch step t - 1 (its alpha~ is also this step's a_{t-1})
-      bl = act ? lbs[(int64_t)(t - 1) * K + j] : N::ninf();
-      by0 = y0g[t - 1];
-      if (two) by1 = y1g[t - 1];
-      bat = act ? aws[(int64_t)(t - 1) * K + j] : R(0);
-    }
-    ObsFeat<R> f0, f1;
-    stat_features<R>(f0, v0, p0.fam);
-    if (two) stat_features<R>(f1, v1, p1.fam);
+    const int p = T - 1 - t;
+    issue(t - (kRing - 1), p + kRing - 1, true);
+    cp_async_wait<kRing - 2>();  // positions p and p + 1 (alpha~_{t-1}) landed
+    const R* sl = ring + (size_t)(p % kRing) * 4 * KM;
+    const R* sn = ring + (size_t)((p + 1) % kRing) * 4 * KM;
+    const R lb = lead ? sl[j] : N::ninf();
+    const R at = lead ? sl[3 * KM + j] : R(0);
+    const R bat = (lead && t >= 1) ? sn[3 * KM + j] : R(0);
     // gamma at t: a_t * exp(r); with it the max of u = lb_t + r for the step
     // to t-1 (one reduction for both)
-    const R q = act ? N::fexp(r) : R(0);
-    R M = act ? lb + r : N::ninf(), gz = at * q;
+    const R qe = act ? N::fexp(r) : R(0);
+    R M = lead ? lb + r : N::ninf(), gz = lead ? at * qe : R(0);
     br.two<false>(M, gz);
-    const R gj = at * q / gz;
-    if (act) {
+    if (lead) {
+      const R gj = at * qe / gz;
+      const R v0 = sl[KM + j], v1 = two ? sl[2 * KM + j] : R(0);
+      ObsFeat<R> f0, f1;
+      stat_features<R>(f0, v0, p0.fam);
+      if (two) stat_features<R>(f1, v1, p1.fam);
       if (outB) outB[(int64_t)t * K + j] = (R)rho + r;
       if (outG) outG[(int64_t)t * K + j] = gj;
       R accs[LOGHMM_NSLOT];
@@ -249,47 +290,46 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
     }
     if (t == 0) break;
     // step to t-1: u = lb_t + r; w = exp(u - M); q_{t-1} = A w
-    const R u = act ? lb + r : N::ninf();
+    const R u = lead ? lb + r : N::ninf();
     const bool fin = M > N::ninf();
-    const R w = (act && fin) ? N::fexp(u - M) : R(0);
+    const R w = (lead && fin) ? N::fexp(u - M) : R(0);
     const R ap = bat;  // alpha~_{t-1}, prefetched above
-    if (act) {
+    if (lead) {
       wv[j] = w;
       apv[j] = ap;  // alpha~_{t-1}, read by every thread below
     }
     __syncthreads();
-    const R acc = act ? reg_dot<R, KM>(Arow, wv) : R(0);
+    R acc = Q::dot(Arow, wv, q);
+    acc = act ? acc : R(0);
     // xi_{t-1}(i, j) = a_{t-1}[i] A_ij w_j / Z, Z = sum_i a_{t-1}[i] q_i;
     // with it the max of log q for the renormalisation (one reduction)
     const R lq = acc > R(0) ? N::flog(acc) : N::ninf();
-    R mq = act ? lq : N::ninf(), Z = ap * acc;
+    R mq = act ? lq : N::ninf(), Z = lead ? ap * acc : R(0);
     br.two<false>(mq, Z);
     const R iz = R(1) / Z;
-    // thread j (as column) accumulates X[i][j] += a_i/Z * w_j
+    // lane (j, q) accumulates X[i][j] += a_i/Z * w_j for its i
     if (act) {
-      const R wz = w * iz;
-      if constexpr (XREG && sizeof(R) == 4) {
+      const R wz = wv[j] * iz;  // w_j, written by lane (j, 0) before the barrier
 #pragma unroll
-        for (int i = 0; i < KM; i += 4) {
-          const float4 q = *reinterpret_cast<const float4*>(apv + i);
-          Xc[i] = fma(q.x, wz, Xc[i]);
-          Xc[i + 1] = fma(q.y, wz, Xc[i + 1]);
-          Xc[i + 2] = fma(q.z, wz, Xc[i + 2]);
-          Xc[i + 3] = fma(q.w, wz, Xc[i + 3]);
+      for (int m = 0; m < Q::NQC; ++m) {
+        const R* pv = apv + (P * m + q) * Q::EPC;
+        if constexpr (sizeof(R) == 4) {
+          const float4 x = *reinterpret_cast<const float4*>(pv);
+          Xc[4 * m] = fma(x.x, wz, Xc[4 * m]);
+          Xc[4 * m + 1] = fma(x.y, wz, Xc[4 * m + 1]);
+          Xc[4 * m + 2] = fma(x.z, wz, Xc[4 * m + 2]);
+          Xc[4 * m + 3] = fma(x.w, wz, Xc[4 * m + 3]);
+        } else {
+          const double2 x = *reinterpret_cast<const double2*>(pv);
+          Xc[2 * m] = fma(x.x, wz, Xc[2 * m]);
+          Xc[2 * m + 1] = fma(x.y, wz, Xc[2 * m + 1]);
         }
-      } else if constexpr (XREG) {
-#pragma unroll
-        for (int i = 0; i < KM; i += 2) {
-          const double2 q = *reinterpret_cast<const double2*>(apv + i);
-          Xc[i] = fma(q.x, wz, Xc[i]);
-          Xc[i + 1] = fma(q.y, wz, Xc[i + 1]);
-        }
-      } else {
-        for (int i = 0; i < K; ++i) Xs[i * 64 + tid] = fma(apv[i], wz, Xs[i * 64 + tid]);
       }
       if (outX)
-        for (int i = 0; i < K; ++i)
-          outX[((int64_t)(t - 1) * K + i) * K + j] = apv[i] * iz * (R)md->A[i * K + j] * w;
+        for (int s = 0; s < NQ; ++s) {
+          const int i = Q::idx(q, s);
+          if (i < K) outX[((int64_t)(t - 1) * K + i) * K + j] = apv[i] * iz * (R)md->A[i * K + j] * wv[j];
+        }
     }
     if (mq > N::ninf()) {
       r = lq - mq;
@@ -300,18 +340,17 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
     // step's wv / apv reads before its writes)
   }
   __syncthreads();
-  const int tid0 = tid;
   // reductions into the partials row
   if (a.partials) {
     double* row = a.partials + b * a.stats_width;
     if (act) {
-      if constexpr (XREG) {
 #pragma unroll
-        for (int i = 0; i < KM; ++i)
-          if (i < K) row[i * K + j] = (double)Xc[i] * md->A[i * K + j];
-      } else {
-        for (int i = 0; i < K; ++i) row[i * K + j] = (double)Xs[i * 64 + tid] * md->A[i * K + j];
+      for (int s = 0; s < NQ; ++s) {
+        const int i = Q::idx(q, s);
+        if (i < K) row[i * K + j] = (double)Xc[s] * md->A[i * K + j];
       }
+    }
+    if (lead) {
       row[K * K + j] = (double)gtot;
       row[K * K + K + j] = (double)g0;
       for (int s = 0; s < 2; ++s)
@@ -321,7 +360,7 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   }
   // dead / nan flags
   __shared__ int s_dead, s_nan, s_oob;
-  if (tid0 == 0) {
+  if (tid == 0) {
     s_dead = INT_MAX;
     s_nan = 0;
     s_oob = 0;
@@ -331,7 +370,7 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   if (nan_seen) s_nan = 1;
   if (oob) s_oob = 1;
   __syncthreads();
-  if (tid0 == 0) {
+  if (tid == 0) {
     a.ll[b] = LL;
     if (a.flags) {
       a.flags[2 * b] = s_dead == INT_MAX ? -1 : s_dead;
@@ -340,27 +379,41 @@ __global__ void __launch_bounds__(64) fb_large_kernel(const FBArgs a, int K, con
   }
 }
 
-// Viterbi, one CTA per sequence, thread j = destination state.  Backpointers
-// go to a byte table in the workspace; thread 0 walks the path with blocks of
-// backpointer rows prefetched into shared memory.
-template <typename R>
-__global__ void __launch_bounds__(64) viterbi_large_kernel(const VitArgs a, int K,
-                                                           uint8_t* backws) {
+// Viterbi, one CTA per sequence, four lanes per destination state j (the
+// Quarter layout of fb_large_kernel): lane q scans the sources i = q, q + 4,
+// ... with log A[i][j] in registers, and the four partial (max, first index)
+// pairs are combined with two xor shuffles, larger value first and the
+// smaller index on ties, which is the reference's first-index argmax
+// (inference.py:204-207) bit for bit.  The score vector is double-buffered in
+// shared memory (one barrier per step) and y is loaded one step ahead.
+// Backpointers go to a byte table in the workspace; thread 0 walks the path
+// with blocks of backpointer rows prefetched into shared memory.
+template <typename R, int KM>
+__global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int K,
+                                                            uint8_t* backws) {
   typedef Num<R> N;
+  constexpr int NQ = KM / 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* LA = reinterpret_cast<R*>(smem_raw);  // K*K log A
-  R* dv = LA + K * K;                      // K
-  uint8_t* bblk = reinterpret_cast<uint8_t*>(dv + K);  // 256*K bytes
+  R* dvb = reinterpret_cast<R*>(smem_raw);                    // [2][KM] scores
+  uint8_t* bblk = reinterpret_cast<uint8_t*>(dvb + 2 * KM);  // 256*K bytes
   __shared__ int s_cur;
   const int tid = threadIdx.x;
+  const int q = tid & 3;
+  const int jt = tid >> 2;
   const int64_t b = blockIdx.x;
   if (b >= a.B) return;
   const int64_t start = a.offsets[b];
   const int T = (int)(a.offsets[b + 1] - start);
-  const bool act = tid < K;
-  const int j = act ? tid : 0;
+  const bool act = jt < K;
+  const bool lead = act && q == 0;
+  const int j = act ? jt : 0;
   const loghmm_model_t* md = a.model;
-  for (int e = tid; e < K * K; e += blockDim.x) LA[e] = (R)md->log_A[e];
+  R la[NQ];  // log A[4s + q][j]
+#pragma unroll
+  for (int s = 0; s < NQ; ++s) {
+    const int i = 4 * s + q;
+    la[s] = (act && i < K) ? (R)md->log_A[i * K + j] : N::ninf();
+  }
   const loghmm_emission_t e0 = md->em[0][j];
   loghmm_emission_t e1;
   const bool two = a.n_streams > 1;
@@ -369,42 +422,58 @@ __global__ void __launch_bounds__(64) viterbi_large_kernel(const VitArgs a, int 
   const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
   uint8_t* bk = backws + start * K;
   bool oob = false;
-  auto logb = [&](int t) -> R {
-    R v = exact_logb<R>(e0, y0g[t], a.lut, a.lut_n, oob);
-    if (two) v = N::add(v, exact_logb<R>(e1, y1g[t], a.lut, a.lut_n, oob));
+  auto logb = [&](R v0, R v1) -> R {
+    R v = exact_logb<R>(e0, v0, a.lut, a.lut_n, oob);
+    if (two) v = N::add(v, exact_logb<R>(e1, v1, a.lut, a.lut_n, oob));
     return v;
   };
-  R delta = act ? N::add((R)md->log_pi[j], logb(0)) : N::ninf();
-  if (act) {
-    dv[j] = delta;
+  if (tid < 2 * KM) dvb[tid] = N::ninf();
+  __syncthreads();
+  if (lead && T > 0) {
+    dvb[j] = N::add((R)md->log_pi[j], logb(y0g[0], two ? y1g[0] : R(0)));
     bk[j] = 0;
     if (a.back) a.back[start * K + j] = 0;
   }
   __syncthreads();
+  int cur = 0;
+  R yn0 = T > 1 ? y0g[1] : R(0), yn1 = (two && T > 1) ? y1g[1] : R(0);
   for (int t = 1; t < T; ++t) {
-    R lb = act ? logb(t) : R(0);
-    R best = N::ninf();
-    int bi = 0;
-    if (act) {
-      best = N::add(dv[0], LA[j]);
-      for (int i = 1; i < K; ++i) {
-        const R c = N::add(dv[i], LA[i * K + j]);
-        if (c > best) {
-          best = c;
-          bi = i;
-        }
+    const R v0 = yn0, v1 = yn1;
+    if (t + 1 < T) {  // prefetch step t + 1
+      yn0 = y0g[t + 1];
+      if (two) yn1 = y1g[t + 1];
+    }
+    const R lb = act ? logb(v0, v1) : R(0);
+    const R* dv = dvb + cur * KM;
+    R best = N::add(dv[q], la[0]);
+    int bi = q;
+#pragma unroll
+    for (int s = 1; s < NQ; ++s) {
+      const R c = N::add(dv[4 * s + q], la[s]);
+      if (c > best) {
+        best = c;
+        bi = 4 * s + q;
       }
     }
-    __syncthreads();
-    if (act) {
-      delta = N::add(best, lb);
-      dv[j] = delta;
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const R ov = __shfl_xor_sync(kFull, best, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    cur ^= 1;
+    if (lead) {
+      dvb[cur * KM + j] = N::add(best, lb);
       bk[(int64_t)t * K + j] = (uint8_t)bi;
       if (a.back) a.back[(start + t) * K + j] = (uint8_t)bi;
     }
     __syncthreads();
   }
   if (tid == 0) {
+    const R* dv = dvb + cur * KM;
     R bv = dv[0];
     int bi = 0;
     for (int i = 1; i < K; ++i)
@@ -425,12 +494,12 @@ __global__ void __launch_bounds__(64) viterbi_large_kernel(const VitArgs a, int 
     for (int e = tid; e < rows * K; e += blockDim.x) bblk[e] = bk[(int64_t)lo * K + e];
     __syncthreads();
     if (tid == 0) {
-      int cur = s_cur;
+      int c = s_cur;
       for (int t = hi; t >= lo; --t) {
-        a.path[start + t] = cur;
-        if (t >= 1) cur = bblk[(t - lo) * K + cur];
+        a.path[start + t] = c;
+        if (t >= 1) c = bblk[(t - lo) * K + c];
       }
-      s_cur = cur;
+      s_cur = c;
     }
     __syncthreads();
   }

@@ -599,6 +599,31 @@ def test_large_k_posteriors_xi_and_viterbi(K, dtype):
     np.testing.assert_allclose(fitted.transitions, A2, atol=1e-9)
 
 
+@pytest.mark.parametrize("K", [13, 33, 64])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_large_k_viterbi_exact_ties(K, dtype):
+    """K > 8 Viterbi with exact candidate ties across the four source lanes of
+    a state (uniform A, states sharing a rate): the combined argmax must be
+    the reference's first index, path and backpointers bit-exact."""
+    rng = np.random.default_rng(900 + K)
+    pi = np.full(K, 1.0 / K)
+    A = np.full((K, K), 1.0 / K)
+    rates = [2.0 + (k % 3) for k in range(K)]  # repeated rates -> tied scores
+    m = H.HmmModel(pi, A, tuple(H.Poisson(r) for r in rates))
+    seqs = [rng.poisson(3.0, n).astype(float) for n in (1, 40, 300)]
+    lp, la = O.model_tables(pi, A)
+    vit = H.viterbi_batch(m, seqs, dtype=dtype, back=True)
+    for b, y in enumerate(seqs):
+        if dtype == "float32":
+            lb32 = O.emission_matrix(to_tuples(m), y.astype(np.float32), np.float32)
+            p, j, bk = O.viterbi(lp.astype(np.float32), la.astype(np.float32), lb32, np.float32)
+        else:
+            p, j, bk = O.viterbi(lp, la, O.emission_matrix(to_tuples(m), y))
+        s = slice(vit.offsets[b], vit.offsets[b + 1])
+        assert np.array_equal(vit.path[s].cpu().numpy(), p)
+        assert np.array_equal(vit.back[s].cpu().numpy().astype(np.int64), bk)
+
+
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_error_semantics_equal_length_batches(dtype):
     """Error paths of the equal-length decomposition (chunk operators + meet in
