@@ -260,7 +260,11 @@ int64_t loghmm_stats_width(int32_t K, int32_t n_streams) {
 size_t loghmm_fb_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N, int64_t max_T) {
   (void)B;
   const int esz = dtype == LOGHMM_F64 ? 8 : 4;
-  if (K > 8) return 2 * align256((size_t)N * K * esz);  // alpha~ store + precomputed log b
+  // alpha~ store + precomputed log b (+ beta~ and w stores and the per-segment
+  // statistics rows of the split fp32 path)
+  if (K > 8)
+    return 4 * align256((size_t)N * K * esz) +
+           align256((size_t)B * kPostSegs * (size_t)loghmm_stats_width(K, 2) * sizeof(double));
   FBGeom g = fb_geom(K, esz, 2, max_T);
   return align256((size_t)B * g.Lmax * kWarp * K * esz);
 }
@@ -404,7 +408,30 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
     } else {
       emission_kernel<float><<<(unsigned)eblocks, 256, 0, st>>>(
           model, (const float*)y0, (const float*)a.y1, N, K, lgamma_lut, lut_n, (float*)lbw);
-      if (KM == 16) LHMM_FBL(float, 16);
+      const char* senv = getenv("LOGHMM_FBL_SPLIT");
+      if (!(senv && atoi(senv) == 0)) {
+        // split path: forward || backward sweeps, then the T-parallel pass
+        SplitWs sw;
+        const size_t nk = align256((size_t)N * K * esz);
+        sw.qws = (float*)((char*)workspace + 2 * nk);
+        sw.wws = (float*)((char*)workspace + 3 * nk);
+        sw.seg_part = (double*)((char*)workspace + 4 * nk);
+        const size_t ssm = (size_t)(2 * KM + 128 + kRing * 4 * KM) * sizeof(float);
+#define LHMM_FBS(KMV)                                                                                   \
+  do {                                                                                                  \
+    if (lps == 4) fb_split_sweep_kernel<KMV, 4><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, (const float*)lbw, sw); \
+    else if (lps == 2) fb_split_sweep_kernel<KMV, 2><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, (const float*)lbw, sw); \
+    else fb_split_sweep_kernel<KMV, 1><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, (const float*)lbw, sw); \
+  } while (0)
+        if (KM == 16) LHMM_FBS(16);
+        else if (KM == 32) LHMM_FBS(32);
+        else LHMM_FBS(64);
+#undef LHMM_FBS
+        const size_t psm = (size_t)(64 * kPostPitch + kPostWarps * 64 + 64 * 64) * sizeof(float) +
+                           (size_t)(2 * 64 * LOGHMM_NSLOT + 2 * 64) * sizeof(double);
+        fb_post_kernel<<<dim3(kPostSegs, (unsigned)B), 32 * kPostWarps, psm, st>>>(a, K, sw);
+        if (partials) fb_fold_kernel<<<(unsigned)B, 256, 0, st>>>(a, K, sw);
+      } else if (KM == 16) LHMM_FBL(float, 16);
       else if (KM == 32) LHMM_FBL(float, 32);
       else LHMM_FBL(float, 64);
     }

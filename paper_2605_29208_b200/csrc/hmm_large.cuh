@@ -379,6 +379,354 @@ __global__ void __launch_bounds__(256) fb_large_kernel(const FBArgs a, int K, co
   }
 }
 
+// ---------------------------------------------------------------------------
+// Split forward-backward for K > 8, fp32 (config 5): the forward and the
+// backward recursions run in separate, concurrent CTAs (grid 2B), and the
+// posteriors, the xi totals and the family statistics are formed afterwards
+// by a T-parallel pass over the stored normalised vectors (fb_post_kernel),
+// so the sequential chain of a sequence is one sweep, not two, and carries no
+// xi / statistics work.
+//   forward CTA  (blockIdx < B): alpha~_t -> aws, log alpha, LL, flags
+//   backward CTA (blockIdx >= B): beta~_t (max 1) -> qws, w_t = b~_t beta~_t
+//                                 (scaled) -> wws, log beta
+// xi_{t-1}(i, j) = alpha~_{t-1}[i] A_ij w_t[j] / Z_t, Z_t = alpha~_{t-1}^T A w_t
+// and gamma_t = alpha~_t beta~_t / sum, exactly the quantities of the fused
+// kernel's backward sweep (training.py:199-210).
+struct SplitWs {
+  float* qws;         // [N, K] beta~ (linear, max 1)
+  float* wws;         // [N, K] w_t
+  double* seg_part;   // [B, kPostSegs, width] per-segment statistics
+};
+constexpr int kPostSegs = 16;
+constexpr int kPostWarps = 8;
+constexpr int kPostPitch = 64 + 4;
+
+template <int KM, int P>
+__global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int K,
+                                                             const float* __restrict__ lbws,
+                                                             const SplitWs sw) {
+  typedef float R;
+  typedef Num<R> N;
+  typedef Quarter<R, KM, P> Q;
+  constexpr int NQ = Q::NQ;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* av = reinterpret_cast<R*>(smem_raw);  // KM
+  R* red = av + KM;                         // 128
+  R* ring = red + 128 + KM;                 // [kRing][4][KM]
+  const int tid = threadIdx.x;
+  const int nw = blockDim.x >> 5;
+  const int q = tid & (P - 1);
+  const int jt = tid / P;
+  const bool bwd = blockIdx.x >= a.B;
+  const int64_t b = bwd ? blockIdx.x - a.B : blockIdx.x;
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  const bool act = jt < K;
+  const bool lead = act && q == 0;
+  const int j = act ? jt : 0;
+  const loghmm_model_t* md = a.model;
+  // column j of A (forward) or row j of A (backward), this lane's elements
+  R Am[NQ];
+#pragma unroll
+  for (int s = 0; s < NQ; ++s) {
+    const int i = Q::idx(q, s);
+    Am[s] = (act && i < K) ? (R)(bwd ? md->A[j * K + i] : md->A[i * K + j]) : R(0);
+  }
+  if (tid < KM) av[tid] = R(0);
+  const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const bool two = a.n_streams > 1;
+  const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  R* aws = reinterpret_cast<R*>(a.alpha_ws) + start * K;
+  const R* __restrict__ lbs = lbws + start * K;
+  __syncthreads();
+  auto issue = [&](int t, int pos) {
+    if (lead) {
+      const bool ok = t >= 0 && t < T;
+      const int tc = ok ? t : 0;
+      R* sl = ring + (size_t)(pos % kRing) * 4 * KM;
+      cp_async<4>(sl + j, lbs + (int64_t)tc * K + j, ok);
+      if (!bwd) {
+        cp_async<4>(sl + KM + j, y0g + tc, ok);
+        if (two) cp_async<4>(sl + 2 * KM + j, y1g + tc, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  BRed<R> br(red, nw);
+#pragma unroll 1
+  for (int d = 0; d < kRing - 1; ++d) issue(bwd ? T - 1 - d : d, d);
+
+  if (!bwd) {
+    R* outA = a.log_alpha ? reinterpret_cast<R*>(a.log_alpha) + start * K : nullptr;
+    const R lpi = (R)md->log_pi[j];
+    bool nan_seen = false;
+    int dead_t = INT_MAX;
+    double lam = 0.0;
+    R a_j = R(0);
+    for (int t = 0; t < T; ++t) {
+      issue(t + kRing - 1, t + kRing - 1);
+      cp_async_wait<kRing - 1>();
+      const R* sl = ring + (size_t)(t % kRing) * 4 * KM;
+      const R lb = lead ? sl[j] : N::ninf();
+      if (lead && (isnan(sl[KM + j]) || (two && isnan(sl[2 * KM + j])))) nan_seen = true;
+      R u;
+      if (t == 0) {
+        u = lpi + lb;
+      } else {
+        const R acc = Q::dot(Am, av, q);
+        u = (acc > R(0) ? N::flog(acc) : N::ninf()) + lb;
+      }
+      if (lead && outA) outA[(int64_t)t * K + j] = (R)lam + u;
+      R M = lead ? u : N::ninf(), mlb = lb;
+      br.two<true>(M, mlb);
+      if (!(mlb > N::ninf()) && t < dead_t) dead_t = t;
+      a_j = (M > N::ninf()) ? N::fexp(u - M) : R(0);
+      if (M > N::ninf()) lam += (double)M;
+      if (lead) {
+        av[j] = a_j;
+        aws[(int64_t)t * K + j] = a_j;
+      }
+      __syncthreads();
+    }
+    cp_async_wait_all();
+    const R s = block_sum(lead ? a_j : R(0), red, nw);
+    const double LL = s > R(0) ? lam + (double)N::flog(s) : -CUDART_INF;
+    __shared__ int s_dead, s_nan;
+    if (tid == 0) {
+      s_dead = INT_MAX;
+      s_nan = 0;
+    }
+    __syncthreads();
+    if (dead_t != INT_MAX) atomicMin(&s_dead, dead_t);
+    if (nan_seen) s_nan = 1;
+    __syncthreads();
+    if (tid == 0) {
+      a.ll[b] = LL;
+      if (a.flags) {
+        a.flags[2 * b] = s_dead == INT_MAX ? -1 : s_dead;
+        a.flags[2 * b + 1] = s_nan ? 1 : 0;
+      }
+    }
+    return;
+  }
+
+  // backward sweep: beta~ and w only
+  R* outB = a.log_beta ? reinterpret_cast<R*>(a.log_beta) + start * K : nullptr;
+  R* qws = sw.qws + start * K;
+  R* wws = sw.wws + start * K;
+  R r = R(0);
+  double rho = 0.0;
+  for (int t = T - 1; t >= 0; --t) {
+    const int p = T - 1 - t;
+    issue(t - (kRing - 1), p + kRing - 1);
+    cp_async_wait<kRing - 1>();
+    const R* sl = ring + (size_t)(p % kRing) * 4 * KM;
+    const R lb = lead ? sl[j] : N::ninf();
+    if (lead) {
+      if (outB) outB[(int64_t)t * K + j] = (R)rho + r;
+      qws[(int64_t)t * K + j] = N::fexp(r);
+    }
+    if (t == 0) break;
+    R M = lead ? lb + r : N::ninf(), dummy = R(0);
+    br.two<true>(M, dummy);
+    const bool fin = M > N::ninf();
+    const R w = (lead && fin) ? N::fexp(lb + r - M) : R(0);
+    if (lead) {
+      av[j] = w;
+      wws[(int64_t)t * K + j] = w;
+    }
+    __syncthreads();
+    R acc = Q::dot(Am, av, q);
+    acc = act ? acc : R(0);
+    const R lq = acc > R(0) ? N::flog(acc) : N::ninf();
+    R mq = act ? lq : N::ninf(), dummy2 = R(0);
+    br.two<true>(mq, dummy2);
+    if (mq > N::ninf()) {
+      r = lq - mq;
+      rho += (fin ? (double)M : 0.0) + (double)mq;
+    }
+  }
+  cp_async_wait_all();
+}
+
+// T-parallel pass: CTA (seg, b) takes steps [seg*len, (seg+1)*len) of
+// sequence b, one warp per step at a time, lane l owning states l and l + 32.
+// gamma_t, the statistics and the xi outer products accumulate in registers,
+// are folded over the warps in fixed order and written as one row per
+// segment; fb_fold_kernel sums the segment rows in order.
+__global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, const SplitWs sw) {
+  typedef float R;
+  typedef Num<R> N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* As = reinterpret_cast<R*>(smem_raw);       // [64][pitch] A rows
+  R* wv = As + 64 * kPostPitch;                 // [warps][64] w_t
+  R* Xs = wv + kPostWarps * 64;                 // [64][64] fold buffer
+  double* sts = reinterpret_cast<double*>(Xs + 64 * 64);  // [2][64][NSLOT] + 2*64 fold
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t b = blockIdx.y;
+  const int seg = blockIdx.x;
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  const int len = (T + kPostSegs - 1) / kPostSegs;
+  const int t0 = seg * len, t1 = min(T, t0 + len);
+  const loghmm_model_t* md = a.model;
+  for (int e = tid; e < 64 * 64; e += blockDim.x) {
+    const int r = e >> 6, c = e & 63;
+    As[r * kPostPitch + c] = (r < K && c < K) ? (R)md->A[r * K + c] : R(0);
+    Xs[e] = R(0);
+  }
+  const bool two = a.n_streams > 1;
+  int is[2];
+  bool act[2];
+  EmP<R> p0[2], p1[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    is[s] = lane + 32 * s;
+    act[s] = is[s] < K;
+    const int ii = act[s] ? is[s] : 0;
+    p0[s] = load_emission<R>(md->em[0][ii]);
+    if (two) p1[s] = load_emission<R>(md->em[1][ii]);
+    else p1[s].fam = LOGHMM_FAM_NONE;
+  }
+  const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  const R* aws = reinterpret_cast<const R*>(a.alpha_ws) + start * K;
+  const R* qws = sw.qws + start * K;
+  const R* wws = sw.wws + start * K;
+  R* outG = a.gamma ? reinterpret_cast<R*>(a.gamma) + start * K : nullptr;
+  R* outX = a.xi ? reinterpret_cast<R*>(a.xi) + (start - b) * (int64_t)K * K : nullptr;
+  R X[2][64];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int c = 0; c < 64; ++c) X[s][c] = R(0);
+  R st[2][2][LOGHMM_NSLOT];
+  R gtot[2] = {R(0), R(0)}, g0[2] = {R(0), R(0)};
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    for (int v = 0; v < 2; ++v)
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][v][qq] = R(0);
+  R* mw = wv + wid * 64;
+  __syncthreads();
+  for (int t = t0 + wid; t < t1; t += kPostWarps) {
+    R at[2], qe[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      at[s] = act[s] ? aws[(int64_t)t * K + is[s]] : R(0);
+      qe[s] = act[s] ? qws[(int64_t)t * K + is[s]] : R(0);
+    }
+    const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
+    const R yv0 = y0g[t], yv1 = two ? y1g[t] : R(0);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (!act[s]) continue;
+      const R gj = at[s] * qe[s] / gz;
+      if (outG) outG[(int64_t)t * K + is[s]] = gj;
+      ObsFeat<R> f0, f1;
+      stat_features<R>(f0, yv0, p0[s].fam);
+      if (two) stat_features<R>(f1, yv1, p1[s].fam);
+      R accs[LOGHMM_NSLOT];
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][0][qq];
+      stat_acc_rt<R>(accs, gj, p0[s], f0);
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][0][qq] = accs[qq];
+      if (two) {
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][1][qq];
+        stat_acc_rt<R>(accs, gj, p1[s], f1);
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][1][qq] = accs[qq];
+      }
+      if (t < T - 1) gtot[s] += gj;
+      if (t == 0) g0[s] = gj;
+    }
+    if (t == 0) continue;
+    // xi_{t-1}: lane row i, q_i = (A w_t)_i, Z = alpha~_{t-1} . q
+    R ap[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      ap[s] = act[s] ? aws[(int64_t)(t - 1) * K + is[s]] : R(0);
+      mw[is[s]] = act[s] ? wws[(int64_t)t * K + is[s]] : R(0);
+    }
+    __syncwarp();
+    R qv[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const R* row = As + is[s] * kPostPitch;
+      R c[4] = {R(0), R(0), R(0), R(0)};
+#pragma unroll
+      for (int i = 0; i < 64; i += 4) {
+        const float4 m = *reinterpret_cast<const float4*>(row + i);
+        const float4 x = *reinterpret_cast<const float4*>(mw + i);
+        c[0] = fma(m.x, x.x, c[0]);
+        c[1] = fma(m.y, x.y, c[1]);
+        c[2] = fma(m.z, x.z, c[2]);
+        c[3] = fma(m.w, x.w, c[3]);
+      }
+      qv[s] = (c[0] + c[1]) + (c[2] + c[3]);
+    }
+    const R Z = warp_sum(ap[0] * qv[0] + ap[1] * qv[1]);
+    const R iz = R(1) / Z;
+    R az[2] = {ap[0] * iz, ap[1] * iz};
+#pragma unroll
+    for (int c = 0; c < 64; c += 4) {
+      const float4 x = *reinterpret_cast<const float4*>(mw + c);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        X[s][c] = fma(az[s], x.x, X[s][c]);
+        X[s][c + 1] = fma(az[s], x.y, X[s][c + 1]);
+        X[s][c + 2] = fma(az[s], x.z, X[s][c + 2]);
+        X[s][c + 3] = fma(az[s], x.w, X[s][c + 3]);
+      }
+    }
+    if (outX) {
+      for (int s = 0; s < 2; ++s)
+        if (act[s])
+          for (int jj = 0; jj < K; ++jj)
+            outX[((int64_t)(t - 1) * K + is[s]) * K + jj] = ap[s] * iz * As[is[s] * kPostPitch + jj] * mw[jj];
+    }
+    __syncwarp();
+  }
+  // fold the warps in order: xi rows, then gamma totals / first gamma / stats
+  double* gts = sts + 2 * 64 * LOGHMM_NSLOT;  // [2][64]: gamma totals, first gamma
+  for (int e = tid; e < 2 * 64 * LOGHMM_NSLOT + 2 * 64; e += blockDim.x) sts[e] = 0.0;
+  __syncthreads();
+  for (int w = 0; w < kPostWarps; ++w) {
+    if (wid == w) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) Xs[is[s] * 64 + c] += X[s][c];
+        for (int v = 0; v < 2; ++v)
+          for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) sts[(v * 64 + is[s]) * LOGHMM_NSLOT + qq] += (double)st[s][v][qq];
+        gts[is[s]] += (double)gtot[s];
+        gts[64 + is[s]] += (double)g0[s];
+      }
+    }
+    __syncthreads();
+  }
+  double* row = sw.seg_part + ((int64_t)b * kPostSegs + seg) * a.stats_width;
+  for (int e = tid; e < K * K; e += blockDim.x) row[e] = (double)Xs[(e / K) * 64 + (e % K)];
+  for (int jj = tid; jj < K; jj += blockDim.x) {
+    row[K * K + jj] = gts[jj];
+    row[K * K + K + jj] = gts[64 + jj];
+    for (int v = 0; v < 2; ++v)
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq)
+        row[K * K + 2 * K + (v * K + jj) * LOGHMM_NSLOT + qq] = sts[(v * 64 + jj) * LOGHMM_NSLOT + qq];
+  }
+}
+
+// partials[b, c] = sum over segments (in order) of seg_part[b, seg, c]; the
+// xi columns are then multiplied by A_ij (as in the fused kernel)
+__global__ void __launch_bounds__(256) fb_fold_kernel(const FBArgs a, int K, const SplitWs sw) {
+  const int64_t b = blockIdx.x;
+  const double* src = sw.seg_part + b * kPostSegs * a.stats_width;
+  double* row = a.partials + b * a.stats_width;
+  for (int64_t c = threadIdx.x; c < a.stats_width; c += blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < kPostSegs; ++s) acc += src[(int64_t)s * a.stats_width + c];
+    if (c < (int64_t)K * K) acc *= a.model->A[c];
+    row[c] = acc;
+  }
+}
+
 // Viterbi, one CTA per sequence, four lanes per destination state j (the
 // Quarter layout of fb_large_kernel): lane q scans the sources i = q, q + 4,
 // ... with log A[i][j] in registers, and the four partial (max, first index)
