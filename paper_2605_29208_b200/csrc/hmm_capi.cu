@@ -246,6 +246,40 @@ static cudaError_t dispatch_fb_chunk(int K, const FBCArgs& a, int cfg, dim3 grid
 
 using namespace lhmm;
 
+// Split large-K forward-backward (hmm_large.cuh): concurrent forward /
+// backward sweep CTAs, the T-parallel posterior pass, the segment fold.
+template <typename R>
+static cudaError_t launch_split(const FBArgs& a, int K, int KM, int lps, int64_t B, int threads,
+                                void* lbw, void* workspace, int64_t N, int esz, bool fold,
+                                cudaStream_t st) {
+  SplitWs sw;
+  const size_t nk = align256((size_t)N * K * esz);
+  sw.qws = (char*)workspace + 2 * nk;
+  sw.wws = (char*)workspace + 3 * nk;
+  sw.seg_part = (double*)((char*)workspace + 4 * nk);
+  const size_t ssm = (size_t)(2 * KM + 128 + kRing * 4 * KM) * sizeof(R);
+  const R* lb = (const R*)lbw;
+#define LHMM_FBS(KMV)                                                                            \
+  do {                                                                                           \
+    if (lps == 4) fb_split_sweep_kernel<R, KMV, 4><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, lb, sw); \
+    else if (lps == 2) fb_split_sweep_kernel<R, KMV, 2><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, lb, sw); \
+    else fb_split_sweep_kernel<R, KMV, 1><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, lb, sw); \
+  } while (0)
+  if (KM == 16) LHMM_FBS(16);
+  else if (KM == 32) LHMM_FBS(32);
+  else LHMM_FBS(64);
+#undef LHMM_FBS
+  const size_t psm = PostGeom<R>::smem();
+  if (psm > 48 * 1024 &&
+      cudaFuncSetAttribute(fb_post_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm) != cudaSuccess)
+    return cudaErrorInvalidValue;
+  const unsigned hz = (K > 32) ? (unsigned)PostGeom<R>::H : 1u;
+  fb_post_kernel<R><<<dim3(kPostSegs, (unsigned)B, hz), 32 * kPostWarps, psm, st>>>(a, K, sw);
+  if (fold) fb_fold_kernel<<<(unsigned)B, 256, 0, st>>>(a, K, sw);
+  return cudaGetLastError();
+}
+
+
 extern "C" {
 
 int32_t loghmm_abi_version(void) { return LOGHMM_ABI_VERSION; }
@@ -301,6 +335,7 @@ int32_t loghmm_emission(int32_t dtype, const loghmm_model_t* h_desc, const loghm
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 
+
 int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
                                 const loghmm_model_t* model, const void* y0, const void* y1,
                                 const int64_t* offsets, int64_t B, int64_t N, int64_t max_T,
@@ -337,7 +372,7 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
   int fams = 0;
   const int cfg = cfg_of(h_desc, &fams);
   a.stream_fams = fams;
-  cudaError_t e;
+  cudaError_t e = cudaSuccess;
   int fbcL = 0;
   size_t fbcW = 0;
   if (use_fbc(K, h_desc->n_streams, B, N, max_T, esz, xi != nullptr, &fbcL, &fbcW)) {
@@ -388,6 +423,11 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
     // 2 and 4 stay selectable for A/B runs
     int lps = 1;
     if (const char* env = getenv("LOGHMM_FBL_LPS")) lps = atoi(env) >= 4 ? 4 : atoi(env) >= 2 ? 2 : 1;
+    // split sweeps + T-parallel pass (default); LOGHMM_FBL_SPLIT=0 selects the
+    // fused one-CTA-per-sequence kernel
+    const char* senv = getenv("LOGHMM_FBL_SPLIT");
+    const bool split = !(senv && atoi(senv) == 0);
+
     const int threads = std::max(32, lps * KM);
     const size_t smem = (size_t)(2 * KM + 128 + kRing * 4 * KM) * esz;
     // log b for the whole batch first (fully parallel), then the sweeps
@@ -402,41 +442,22 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
     if (dtype == LOGHMM_F64) {
       emission_kernel<double><<<(unsigned)eblocks, 256, 0, st>>>(
           model, (const double*)y0, (const double*)a.y1, N, K, lgamma_lut, lut_n, (double*)lbw);
-      if (KM == 16) LHMM_FBL(double, 16);
+      if (split) e = launch_split<double>(a, K, KM, lps, B, threads, lbw, workspace, N, esz, partials != nullptr, st);
+      else if (KM == 16) LHMM_FBL(double, 16);
       else if (KM == 32) LHMM_FBL(double, 32);
       else LHMM_FBL(double, 64);
     } else {
       emission_kernel<float><<<(unsigned)eblocks, 256, 0, st>>>(
           model, (const float*)y0, (const float*)a.y1, N, K, lgamma_lut, lut_n, (float*)lbw);
-      const char* senv = getenv("LOGHMM_FBL_SPLIT");
-      if (!(senv && atoi(senv) == 0)) {
-        // split path: forward || backward sweeps, then the T-parallel pass
-        SplitWs sw;
-        const size_t nk = align256((size_t)N * K * esz);
-        sw.qws = (float*)((char*)workspace + 2 * nk);
-        sw.wws = (float*)((char*)workspace + 3 * nk);
-        sw.seg_part = (double*)((char*)workspace + 4 * nk);
-        const size_t ssm = (size_t)(2 * KM + 128 + kRing * 4 * KM) * sizeof(float);
-#define LHMM_FBS(KMV)                                                                                   \
-  do {                                                                                                  \
-    if (lps == 4) fb_split_sweep_kernel<KMV, 4><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, (const float*)lbw, sw); \
-    else if (lps == 2) fb_split_sweep_kernel<KMV, 2><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, (const float*)lbw, sw); \
-    else fb_split_sweep_kernel<KMV, 1><<<(unsigned)(2 * B), threads, ssm, st>>>(a, K, (const float*)lbw, sw); \
-  } while (0)
-        if (KM == 16) LHMM_FBS(16);
-        else if (KM == 32) LHMM_FBS(32);
-        else LHMM_FBS(64);
-#undef LHMM_FBS
-        const size_t psm = (size_t)(64 * kPostPitch + kPostWarps * 64 + 64 * 64) * sizeof(float) +
-                           (size_t)(2 * 64 * LOGHMM_NSLOT + 2 * 64) * sizeof(double);
-        fb_post_kernel<<<dim3(kPostSegs, (unsigned)B), 32 * kPostWarps, psm, st>>>(a, K, sw);
-        if (partials) fb_fold_kernel<<<(unsigned)B, 256, 0, st>>>(a, K, sw);
+      if (split) {
+        e = launch_split<float>(a, K, KM, lps, B, threads, lbw, workspace, N, esz, partials != nullptr, st);
       } else if (KM == 16) LHMM_FBL(float, 16);
       else if (KM == 32) LHMM_FBL(float, 32);
       else LHMM_FBL(float, 64);
     }
 #undef LHMM_FBL
-    e = cudaGetLastError();
+    const cudaError_t e2 = cudaGetLastError();
+    if (e == cudaSuccess) e = e2;
   }
   return e == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }

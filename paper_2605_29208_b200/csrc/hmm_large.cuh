@@ -393,19 +393,18 @@ __global__ void __launch_bounds__(256) fb_large_kernel(const FBArgs a, int K, co
 // and gamma_t = alpha~_t beta~_t / sum, exactly the quantities of the fused
 // kernel's backward sweep (training.py:199-210).
 struct SplitWs {
-  float* qws;         // [N, K] beta~ (linear, max 1)
-  float* wws;         // [N, K] w_t
+  void* qws;          // [N, K] beta~ (linear, max 1)
+  void* wws;          // [N, K] w_t
   double* seg_part;   // [B, kPostSegs, width] per-segment statistics
 };
 constexpr int kPostSegs = 16;
 constexpr int kPostWarps = 8;
 constexpr int kPostPitch = 64 + 4;
 
-template <int KM, int P>
+template <typename R, int KM, int P>
 __global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int K,
-                                                             const float* __restrict__ lbws,
+                                                             const R* __restrict__ lbws,
                                                              const SplitWs sw) {
-  typedef float R;
   typedef Num<R> N;
   typedef Quarter<R, KM, P> Q;
   constexpr int NQ = Q::NQ;
@@ -444,10 +443,10 @@ __global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int
       const bool ok = t >= 0 && t < T;
       const int tc = ok ? t : 0;
       R* sl = ring + (size_t)(pos % kRing) * 4 * KM;
-      cp_async<4>(sl + j, lbs + (int64_t)tc * K + j, ok);
+      cp_async<sizeof(R)>(sl + j, lbs + (int64_t)tc * K + j, ok);
       if (!bwd) {
-        cp_async<4>(sl + KM + j, y0g + tc, ok);
-        if (two) cp_async<4>(sl + 2 * KM + j, y1g + tc, ok);
+        cp_async<sizeof(R)>(sl + KM + j, y0g + tc, ok);
+        if (two) cp_async<sizeof(R)>(sl + 2 * KM + j, y1g + tc, ok);
       }
     }
     cp_async_commit();
@@ -512,8 +511,8 @@ __global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int
 
   // backward sweep: beta~ and w only
   R* outB = a.log_beta ? reinterpret_cast<R*>(a.log_beta) + start * K : nullptr;
-  R* qws = sw.qws + start * K;
-  R* wws = sw.wws + start * K;
+  R* qws = reinterpret_cast<R*>(sw.qws) + start * K;
+  R* wws = reinterpret_cast<R*>(sw.wws) + start * K;
   R r = R(0);
   double rho = 0.0;
   for (int t = T - 1; t >= 0; --t) {
@@ -549,22 +548,64 @@ __global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int
   cp_async_wait_all();
 }
 
-// T-parallel pass: CTA (seg, b) takes steps [seg*len, (seg+1)*len) of
-// sequence b, one warp per step at a time, lane l owning states l and l + 32.
-// gamma_t, the statistics and the xi outer products accumulate in registers,
-// are folded over the warps in fixed order and written as one row per
-// segment; fb_fold_kernel sums the segment rows in order.
+// T-parallel pass: CTA (seg, b, h) takes steps [seg*len, (seg+1)*len) of
+// sequence b, one warp per step at a time.  Every lane evaluates gamma_t and
+// the xi normaliser Z_t for states l and l + 32; the xi outer-product rows it
+// accumulates in registers are RPL of them (fp32: both, h = 0; fp64: row
+// l + 32h, two CTAs per segment), and the h = 0 CTA accumulates the
+// statistics.  Warps are folded in fixed order and each CTA writes its
+// columns of the segment row; fb_fold_kernel sums the segment rows in order.
+template <typename R>
+struct PostGeom {
+  static constexpr int RPL = sizeof(R) == 4 ? 2 : 1;  // xi rows per lane
+  static constexpr int H = 2 / RPL;                   // CTAs per segment
+  static constexpr int PITCH = 64 + 16 / (int)sizeof(R) * 1;  // padded A row (elements)
+  static constexpr size_t smem() {
+    return (size_t)(64 * PITCH + kPostWarps * 64 + 64 * 64) * sizeof(R) +
+           (size_t)(2 * 64 * LOGHMM_NSLOT + 2 * 64) * sizeof(double);
+  }
+};
+
+template <typename R>
+__device__ __forceinline__ R row_dot64(const R* __restrict__ row, const R* __restrict__ v) {
+  R c[4] = {R(0), R(0), R(0), R(0)};
+  if constexpr (sizeof(R) == 4) {
+#pragma unroll
+    for (int i = 0; i < 64; i += 4) {
+      const float4 m = *reinterpret_cast<const float4*>(row + i);
+      const float4 x = *reinterpret_cast<const float4*>(v + i);
+      c[0] = fma(m.x, x.x, c[0]);
+      c[1] = fma(m.y, x.y, c[1]);
+      c[2] = fma(m.z, x.z, c[2]);
+      c[3] = fma(m.w, x.w, c[3]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      const double2 m = *reinterpret_cast<const double2*>(row + i);
+      const double2 x = *reinterpret_cast<const double2*>(v + i);
+      c[(i >> 1) & 3] = fma(m.x, x.x, c[(i >> 1) & 3]);
+      c[((i >> 1) + 2) & 3] = fma(m.y, x.y, c[((i >> 1) + 2) & 3]);
+    }
+  }
+  return (c[0] + c[1]) + (c[2] + c[3]);
+}
+
+template <typename R>
 __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, const SplitWs sw) {
-  typedef float R;
   typedef Num<R> N;
+  typedef PostGeom<R> PG;
+  constexpr int RPL = PG::RPL;
+  constexpr int PITCH = PG::PITCH;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* As = reinterpret_cast<R*>(smem_raw);       // [64][pitch] A rows
-  R* wv = As + 64 * kPostPitch;                 // [warps][64] w_t
-  R* Xs = wv + kPostWarps * 64;                 // [64][64] fold buffer
-  double* sts = reinterpret_cast<double*>(Xs + 64 * 64);  // [2][64][NSLOT] + 2*64 fold
+  R* As = reinterpret_cast<R*>(smem_raw);  // [64][PITCH] A rows
+  R* wv = As + 64 * PITCH;                 // [warps][64] w_t
+  R* Xs = wv + kPostWarps * 64;            // [64][64] fold buffer
+  double* sts = reinterpret_cast<double*>(Xs + 64 * 64);  // [2][64][NSLOT] + [2][64]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t b = blockIdx.y;
   const int seg = blockIdx.x;
+  const int h = blockIdx.z;
   const int64_t start = a.offsets[b];
   const int T = (int)(a.offsets[b + 1] - start);
   const int len = (T + kPostSegs - 1) / kPostSegs;
@@ -572,10 +613,11 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
   const loghmm_model_t* md = a.model;
   for (int e = tid; e < 64 * 64; e += blockDim.x) {
     const int r = e >> 6, c = e & 63;
-    As[r * kPostPitch + c] = (r < K && c < K) ? (R)md->A[r * K + c] : R(0);
+    As[r * PITCH + c] = (r < K && c < K) ? (R)md->A[r * K + c] : R(0);
     Xs[e] = R(0);
   }
   const bool two = a.n_streams > 1;
+  const bool do_stats = h == 0;
   int is[2];
   bool act[2];
   EmP<R> p0[2], p1[2];
@@ -591,13 +633,13 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
   const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
   const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
   const R* aws = reinterpret_cast<const R*>(a.alpha_ws) + start * K;
-  const R* qws = sw.qws + start * K;
-  const R* wws = sw.wws + start * K;
-  R* outG = a.gamma ? reinterpret_cast<R*>(a.gamma) + start * K : nullptr;
+  const R* qws = reinterpret_cast<const R*>(sw.qws) + start * K;
+  const R* wws = reinterpret_cast<const R*>(sw.wws) + start * K;
+  R* outG = (a.gamma && do_stats) ? reinterpret_cast<R*>(a.gamma) + start * K : nullptr;
   R* outX = a.xi ? reinterpret_cast<R*>(a.xi) + (start - b) * (int64_t)K * K : nullptr;
-  R X[2][64];
+  R X[RPL][64];
 #pragma unroll
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < RPL; ++s)
 #pragma unroll
     for (int c = 0; c < 64; ++c) X[s][c] = R(0);
   R st[2][2][LOGHMM_NSLOT];
@@ -609,78 +651,83 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
   R* mw = wv + wid * 64;
   __syncthreads();
   for (int t = t0 + wid; t < t1; t += kPostWarps) {
-    R at[2], qe[2];
+    if (do_stats) {
+      R at[2], qe[2];
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      at[s] = act[s] ? aws[(int64_t)t * K + is[s]] : R(0);
-      qe[s] = act[s] ? qws[(int64_t)t * K + is[s]] : R(0);
-    }
-    const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
-    const R yv0 = y0g[t], yv1 = two ? y1g[t] : R(0);
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (!act[s]) continue;
-      const R gj = at[s] * qe[s] / gz;
-      if (outG) outG[(int64_t)t * K + is[s]] = gj;
-      ObsFeat<R> f0, f1;
-      stat_features<R>(f0, yv0, p0[s].fam);
-      if (two) stat_features<R>(f1, yv1, p1[s].fam);
-      R accs[LOGHMM_NSLOT];
-      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][0][qq];
-      stat_acc_rt<R>(accs, gj, p0[s], f0);
-      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][0][qq] = accs[qq];
-      if (two) {
-        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][1][qq];
-        stat_acc_rt<R>(accs, gj, p1[s], f1);
-        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][1][qq] = accs[qq];
+      for (int s = 0; s < 2; ++s) {
+        at[s] = act[s] ? aws[(int64_t)t * K + is[s]] : R(0);
+        qe[s] = act[s] ? qws[(int64_t)t * K + is[s]] : R(0);
       }
-      if (t < T - 1) gtot[s] += gj;
-      if (t == 0) g0[s] = gj;
+      const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
+      const R yv0 = y0g[t], yv1 = two ? y1g[t] : R(0);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (!act[s]) continue;
+        const R gj = at[s] * qe[s] / gz;
+        if (outG) outG[(int64_t)t * K + is[s]] = gj;
+        ObsFeat<R> f0, f1;
+        stat_features<R>(f0, yv0, p0[s].fam);
+        if (two) stat_features<R>(f1, yv1, p1[s].fam);
+        R accs[LOGHMM_NSLOT];
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][0][qq];
+        stat_acc_rt<R>(accs, gj, p0[s], f0);
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][0][qq] = accs[qq];
+        if (two) {
+          for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][1][qq];
+          stat_acc_rt<R>(accs, gj, p1[s], f1);
+          for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][1][qq] = accs[qq];
+        }
+        if (t < T - 1) gtot[s] += gj;
+        if (t == 0) g0[s] = gj;
+      }
     }
     if (t == 0) continue;
-    // xi_{t-1}: lane row i, q_i = (A w_t)_i, Z = alpha~_{t-1} . q
-    R ap[2];
+    // xi_{t-1}: q_i = (A w_t)_i, Z = alpha~_{t-1} . q over all rows
+    R ap[2], qv[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       ap[s] = act[s] ? aws[(int64_t)(t - 1) * K + is[s]] : R(0);
       mw[is[s]] = act[s] ? wws[(int64_t)t * K + is[s]] : R(0);
     }
     __syncwarp();
-    R qv[2];
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const R* row = As + is[s] * kPostPitch;
-      R c[4] = {R(0), R(0), R(0), R(0)};
-#pragma unroll
-      for (int i = 0; i < 64; i += 4) {
-        const float4 m = *reinterpret_cast<const float4*>(row + i);
-        const float4 x = *reinterpret_cast<const float4*>(mw + i);
-        c[0] = fma(m.x, x.x, c[0]);
-        c[1] = fma(m.y, x.y, c[1]);
-        c[2] = fma(m.z, x.z, c[2]);
-        c[3] = fma(m.w, x.w, c[3]);
-      }
-      qv[s] = (c[0] + c[1]) + (c[2] + c[3]);
-    }
+    for (int s = 0; s < 2; ++s) qv[s] = row_dot64<R>(As + is[s] * PITCH, mw);
     const R Z = warp_sum(ap[0] * qv[0] + ap[1] * qv[1]);
     const R iz = R(1) / Z;
-    R az[2] = {ap[0] * iz, ap[1] * iz};
+    R az[RPL];
 #pragma unroll
-    for (int c = 0; c < 64; c += 4) {
-      const float4 x = *reinterpret_cast<const float4*>(mw + c);
+    for (int s = 0; s < RPL; ++s) az[s] = ap[s + h * RPL] * iz;  // h * RPL is 0 or 1
+    if constexpr (sizeof(R) == 4) {
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        X[s][c] = fma(az[s], x.x, X[s][c]);
-        X[s][c + 1] = fma(az[s], x.y, X[s][c + 1]);
-        X[s][c + 2] = fma(az[s], x.z, X[s][c + 2]);
-        X[s][c + 3] = fma(az[s], x.w, X[s][c + 3]);
+      for (int c = 0; c < 64; c += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(mw + c);
+#pragma unroll
+        for (int s = 0; s < RPL; ++s) {
+          X[s][c] = fma(az[s], x.x, X[s][c]);
+          X[s][c + 1] = fma(az[s], x.y, X[s][c + 1]);
+          X[s][c + 2] = fma(az[s], x.z, X[s][c + 2]);
+          X[s][c + 3] = fma(az[s], x.w, X[s][c + 3]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 64; c += 2) {
+        const double2 x = *reinterpret_cast<const double2*>(mw + c);
+#pragma unroll
+        for (int s = 0; s < RPL; ++s) {
+          X[s][c] = fma(az[s], x.x, X[s][c]);
+          X[s][c + 1] = fma(az[s], x.y, X[s][c + 1]);
+        }
       }
     }
     if (outX) {
-      for (int s = 0; s < 2; ++s)
-        if (act[s])
+#pragma unroll
+      for (int s = 0; s < RPL; ++s) {
+        const int ii = is[s + h * RPL];
+        if (ii < K)
           for (int jj = 0; jj < K; ++jj)
-            outX[((int64_t)(t - 1) * K + is[s]) * K + jj] = ap[s] * iz * As[is[s] * kPostPitch + jj] * mw[jj];
+            outX[((int64_t)(t - 1) * K + ii) * K + jj] = ap[s + h * RPL] * iz * As[ii * PITCH + jj] * mw[jj];
+      }
     }
     __syncwarp();
   }
@@ -691,9 +738,13 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
   for (int w = 0; w < kPostWarps; ++w) {
     if (wid == w) {
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < RPL; ++s) {
+        const int ii = is[s + h * RPL];
 #pragma unroll
-        for (int c = 0; c < 64; ++c) Xs[is[s] * 64 + c] += X[s][c];
+        for (int c = 0; c < 64; ++c) Xs[ii * 64 + c] += X[s][c];
+      }
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
         for (int v = 0; v < 2; ++v)
           for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) sts[(v * 64 + is[s]) * LOGHMM_NSLOT + qq] += (double)st[s][v][qq];
         gts[is[s]] += (double)gtot[s];
@@ -703,13 +754,19 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
     __syncthreads();
   }
   double* row = sw.seg_part + ((int64_t)b * kPostSegs + seg) * a.stats_width;
-  for (int e = tid; e < K * K; e += blockDim.x) row[e] = (double)Xs[(e / K) * 64 + (e % K)];
-  for (int jj = tid; jj < K; jj += blockDim.x) {
-    row[K * K + jj] = gts[jj];
-    row[K * K + K + jj] = gts[64 + jj];
-    for (int v = 0; v < 2; ++v)
-      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq)
-        row[K * K + 2 * K + (v * K + jj) * LOGHMM_NSLOT + qq] = sts[(v * 64 + jj) * LOGHMM_NSLOT + qq];
+  const int r0 = h * 32 * RPL, r1 = min(K, r0 + 32 * RPL);  // this CTA's xi rows
+  for (int e = tid; e < (r1 - r0) * K; e += blockDim.x) {
+    const int i = r0 + e / K, jj = e % K;
+    row[i * K + jj] = (double)Xs[i * 64 + jj];
+  }
+  if (do_stats) {
+    for (int jj = tid; jj < K; jj += blockDim.x) {
+      row[K * K + jj] = gts[jj];
+      row[K * K + K + jj] = gts[64 + jj];
+      for (int v = 0; v < 2; ++v)
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq)
+          row[K * K + 2 * K + (v * K + jj) * LOGHMM_NSLOT + qq] = sts[(v * 64 + jj) * LOGHMM_NSLOT + qq];
+    }
   }
 }
 
