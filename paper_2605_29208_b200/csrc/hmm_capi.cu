@@ -515,10 +515,16 @@ int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm
   } else {
     const int esz = dtype == LOGHMM_F64 ? 8 : 4;
     const int KM = K <= 16 ? 16 : K <= 32 ? 32 : 64;
-    const int threads = 4 * KM;  // four lanes per destination state
+    int vlps = 4;  // lanes per destination state (LOGHMM_VL_LPS: 1, 2 or 4)
+    if (const char* env = getenv("LOGHMM_VL_LPS")) vlps = atoi(env) >= 4 ? 4 : atoi(env) >= 2 ? 2 : 1;
+    const int threads = std::max(32, vlps * KM);
     const size_t smem = (size_t)(2 * KM) * esz + 256 * (size_t)K;
 #define LHMM_VL(RR, KMV)                                                                         \
-  viterbi_large_kernel<RR, KMV><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace)
+  do {                                                                                           \
+    if (vlps == 4) viterbi_large_kernel<RR, KMV, 4><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace); \
+    else if (vlps == 2) viterbi_large_kernel<RR, KMV, 2><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace); \
+    else viterbi_large_kernel<RR, KMV, 1><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace); \
+  } while (0)
     if (dtype == LOGHMM_F64) {
       if (KM == 16) LHMM_VL(double, 16);
       else if (KM == 32) LHMM_VL(double, 32);

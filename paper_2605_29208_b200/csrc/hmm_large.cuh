@@ -793,18 +793,18 @@ __global__ void __launch_bounds__(256) fb_fold_kernel(const FBArgs a, int K, con
 // shared memory (one barrier per step) and y is loaded one step ahead.
 // Backpointers go to a byte table in the workspace; thread 0 walks the path
 // with blocks of backpointer rows prefetched into shared memory.
-template <typename R, int KM>
+template <typename R, int KM, int P>
 __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int K,
                                                             uint8_t* backws) {
   typedef Num<R> N;
-  constexpr int NQ = KM / 4;
+  constexpr int NQ = KM / P;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* dvb = reinterpret_cast<R*>(smem_raw);                    // [2][KM] scores
   uint8_t* bblk = reinterpret_cast<uint8_t*>(dvb + 2 * KM);  // 256*K bytes
   __shared__ int s_cur;
   const int tid = threadIdx.x;
-  const int q = tid & 3;
-  const int jt = tid >> 2;
+  const int q = tid & (P - 1);
+  const int jt = tid / P;
   const int64_t b = blockIdx.x;
   if (b >= a.B) return;
   const int64_t start = a.offsets[b];
@@ -813,10 +813,10 @@ __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int
   const bool lead = act && q == 0;
   const int j = act ? jt : 0;
   const loghmm_model_t* md = a.model;
-  R la[NQ];  // log A[4s + q][j]
+  R la[NQ];  // log A[P s + q][j]
 #pragma unroll
   for (int s = 0; s < NQ; ++s) {
-    const int i = 4 * s + q;
+    const int i = P * s + q;
     la[s] = (act && i < K) ? (R)md->log_A[i * K + j] : N::ninf();
   }
   const loghmm_emission_t e0 = md->em[0][j];
@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int
     if (two) v = N::add(v, exact_logb<R>(e1, v1, a.lut, a.lut_n, oob));
     return v;
   };
-  if (tid < 2 * KM) dvb[tid] = N::ninf();
+  for (int e = tid; e < 2 * KM; e += blockDim.x) dvb[e] = N::ninf();
   __syncthreads();
   if (lead && T > 0) {
     dvb[j] = N::add((R)md->log_pi[j], logb(y0g[0], two ? y1g[0] : R(0)));
@@ -854,14 +854,14 @@ __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int
     int bi = q;
 #pragma unroll
     for (int s = 1; s < NQ; ++s) {
-      const R c = N::add(dv[4 * s + q], la[s]);
+      const R c = N::add(dv[P * s + q], la[s]);
       if (c > best) {
         best = c;
-        bi = 4 * s + q;
+        bi = P * s + q;
       }
     }
 #pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
+    for (int o = 1; o < P; o <<= 1) {
       const R ov = __shfl_xor_sync(kFull, best, o);
       const int oi = __shfl_xor_sync(kFull, bi, o);
       if (ov > best || (ov == best && oi < bi)) {
