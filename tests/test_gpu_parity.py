@@ -599,6 +599,38 @@ def test_large_k_posteriors_xi_and_viterbi(K, dtype):
     np.testing.assert_allclose(fitted.transitions, A2, atol=1e-9)
 
 
+@pytest.mark.parametrize("K", [12, 33])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_large_k_short_sequences_split_pass(K, dtype):
+    """Large-K forward-backward on sequences shorter than the T-parallel
+    pass's segment count (T = 1, 2, 15, 17: empty and one-step segments) and
+    a long one, through the statistics of one Baum-Welch iteration."""
+    rng = np.random.default_rng(700 + K)
+    pi = rng.dirichlet(np.ones(K))
+    A = rng.dirichlet(np.ones(K), size=K) * 0.3 + 0.7 * np.eye(K)
+    A /= A.sum(1, keepdims=True)
+    m = H.HmmModel(pi, A, tuple(H.Poisson(float(r)) for r in np.linspace(0.5, 9.0, K)))
+    seqs = [rng.poisson(4.0, n).astype(float) for n in (1, 2, 15, 17, 400)]
+    r = H.posteriors_batch(m, seqs, dtype=dtype, include_xi=True)
+    lp, la = O.model_tables(pi, A)
+    tol = 1e-9 if dtype == "float64" else 1e-5
+    X_ = r.xi.cpu().numpy().astype(np.float64)
+    for b, y in enumerate(seqs):
+        o = O.posteriors(lp, la, O.emission_matrix(to_tuples(m), y), include_xi=True)
+        s = slice(r.offsets[b], r.offsets[b + 1])
+        xs = slice(r.offsets[b] - b, r.offsets[b + 1] - b - 1)
+        assert r.log_likelihood[b].item() == pytest.approx(o["ll"], rel=1e-9 if dtype == "float64" else 1e-4)
+        np.testing.assert_allclose(r.gamma[s].double().cpu().numpy(), o["gamma"], atol=tol)
+        np.testing.assert_allclose(r.log_alpha[s].double().cpu().numpy(), o["log_alpha"], rtol=1e-9 if dtype == "float64" else 1e-5, atol=tol)
+        np.testing.assert_allclose(r.log_beta[s].double().cpu().numpy(), o["log_beta"], rtol=1e-9 if dtype == "float64" else 1e-5, atol=tol)
+        if len(y) > 1:
+            np.testing.assert_allclose(X_[xs], o["xi"], atol=tol)
+    fitted, rep = H.baum_welch(m, seqs, H.TrainingConfig(max_iterations=2, rel_tol=1e-300), dtype=dtype)
+    pi2, A2, em2, trace, _, _ = O.baum_welch(pi, A, to_tuples(m), seqs, 2)
+    np.testing.assert_allclose(rep.log_likelihood_trace, trace, rtol=1e-9 if dtype == "float64" else 1e-4)
+    np.testing.assert_allclose(fitted.transitions, A2, atol=1e-9 if dtype == "float64" else 1e-4)
+
+
 @pytest.mark.parametrize("K", [13, 33, 64])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_large_k_viterbi_exact_ties(K, dtype):
