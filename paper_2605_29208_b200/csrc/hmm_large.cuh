@@ -548,20 +548,13 @@ __global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int
   cp_async_wait_all();
 }
 
-// T-parallel pass: CTA (seg, b, h) takes steps [seg*len, (seg+1)*len) of
-// sequence b, one warp per step at a time.  Every lane evaluates gamma_t and
-// the xi normaliser Z_t for states l and l + 32; the xi outer-product rows it
-// accumulates in registers are RPL of them (fp32: both, h = 0; fp64: row
-// l + 32h, two CTAs per segment), and the h = 0 CTA accumulates the
-// statistics.  Warps are folded in fixed order and each CTA writes its
-// columns of the segment row; fb_fold_kernel sums the segment rows in order.
 template <typename R>
 struct PostGeom {
-  static constexpr int RPL = sizeof(R) == 4 ? 2 : 1;  // xi rows per lane
-  static constexpr int H = 2 / RPL;                   // CTAs per segment
-  static constexpr int PITCH = 64 + 16 / (int)sizeof(R) * 1;  // padded A row (elements)
+  static constexpr int H = 1;                               // CTAs per segment
+  static constexpr int PITCH = 64 + 16 / (int)sizeof(R);    // padded A row (elements)
+  static constexpr int TC = 32;                             // steps per tile chunk
   static constexpr size_t smem() {
-    return (size_t)(64 * PITCH + kPostWarps * 64 + 64 * 64) * sizeof(R) +
+    return (size_t)(64 * PITCH + kPostWarps * 64 + 2 * TC * 64) * sizeof(R) +
            (size_t)(2 * 64 * LOGHMM_NSLOT + 2 * 64) * sizeof(double);
   }
 };
@@ -591,21 +584,29 @@ __device__ __forceinline__ R row_dot64(const R* __restrict__ row, const R* __res
   return (c[0] + c[1]) + (c[2] + c[3]);
 }
 
+// T-parallel pass: CTA (seg, b) takes steps [seg*len, (seg+1)*len) of
+// sequence b in chunks of TC steps.  Phase 1, one warp per step (lane l owns
+// states l and l + 32): gamma_t and the statistics, and for xi the row
+// alpha~_{t-1}/Z_t and w_t into two [TC][64] shared tiles, Z_t =
+// alpha~_{t-1}^T A w_t.  Phase 2: the CTA accumulates the 64x64 xi outer
+// products of the chunk as a tiled rank-TC update (4x4 register tile per
+// thread).  The statistics are folded over the warps in fixed order; each
+// CTA writes one segment row, fb_fold_kernel sums the segment rows in order.
 template <typename R>
-__global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, const SplitWs sw) {
+__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) fb_post_kernel(const FBArgs a, int K, const SplitWs sw) {
   typedef Num<R> N;
   typedef PostGeom<R> PG;
-  constexpr int RPL = PG::RPL;
   constexpr int PITCH = PG::PITCH;
+  constexpr int TC = PG::TC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* As = reinterpret_cast<R*>(smem_raw);  // [64][PITCH] A rows
   R* wv = As + 64 * PITCH;                 // [warps][64] w_t
-  R* Xs = wv + kPostWarps * 64;            // [64][64] fold buffer
-  double* sts = reinterpret_cast<double*>(Xs + 64 * 64);  // [2][64][NSLOT] + [2][64]
+  R* Ta = wv + kPostWarps * 64;            // [TC][64] alpha~_{t-1} / Z_t
+  R* Tw = Ta + TC * 64;                    // [TC][64] w_t
+  double* sts = reinterpret_cast<double*>(Tw + TC * 64);  // [2][64][NSLOT] + [2][64]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t b = blockIdx.y;
   const int seg = blockIdx.x;
-  const int h = blockIdx.z;
   const int64_t start = a.offsets[b];
   const int T = (int)(a.offsets[b + 1] - start);
   const int len = (T + kPostSegs - 1) / kPostSegs;
@@ -614,10 +615,8 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
   for (int e = tid; e < 64 * 64; e += blockDim.x) {
     const int r = e >> 6, c = e & 63;
     As[r * PITCH + c] = (r < K && c < K) ? (R)md->A[r * K + c] : R(0);
-    Xs[e] = R(0);
   }
   const bool two = a.n_streams > 1;
-  const bool do_stats = h == 0;
   int is[2];
   bool act[2];
   EmP<R> p0[2], p1[2];
@@ -635,13 +634,15 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
   const R* aws = reinterpret_cast<const R*>(a.alpha_ws) + start * K;
   const R* qws = reinterpret_cast<const R*>(sw.qws) + start * K;
   const R* wws = reinterpret_cast<const R*>(sw.wws) + start * K;
-  R* outG = (a.gamma && do_stats) ? reinterpret_cast<R*>(a.gamma) + start * K : nullptr;
+  R* outG = a.gamma ? reinterpret_cast<R*>(a.gamma) + start * K : nullptr;
   R* outX = a.xi ? reinterpret_cast<R*>(a.xi) + (start - b) * (int64_t)K * K : nullptr;
-  R X[RPL][64];
+  // phase-2 tile: rows 4*ti .. 4*ti+3, columns 4*tj .. 4*tj+3
+  const int ti = tid >> 4, tj = tid & 15;
+  R X[4][4];
 #pragma unroll
-  for (int s = 0; s < RPL; ++s)
+  for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int c = 0; c < 64; ++c) X[s][c] = R(0);
+    for (int c = 0; c < 4; ++c) X[r][c] = R(0);
   R st[2][2][LOGHMM_NSLOT];
   R gtot[2] = {R(0), R(0)}, g0[2] = {R(0), R(0)};
 #pragma unroll
@@ -650,99 +651,117 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
       for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][v][qq] = R(0);
   R* mw = wv + wid * 64;
   __syncthreads();
-  for (int t = t0 + wid; t < t1; t += kPostWarps) {
-    if (do_stats) {
-      R at[2], qe[2];
+  for (int c0 = t0; c0 < t1; c0 += TC) {
+    for (int tt = wid; tt < TC; tt += kPostWarps) {
+      const int t = c0 + tt;
+      R* ta = Ta + tt * 64;
+      R* tw = Tw + tt * 64;
+      if (t >= t1) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          ta[is[s]] = R(0);
+          tw[is[s]] = R(0);
+        }
+        continue;
+      }
+      {
+        R at[2], qe[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          at[s] = act[s] ? aws[(int64_t)t * K + is[s]] : R(0);
+          qe[s] = act[s] ? qws[(int64_t)t * K + is[s]] : R(0);
+        }
+        const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
+        const R yv0 = y0g[t], yv1 = two ? y1g[t] : R(0);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (!act[s]) continue;
+          const R gj = at[s] * qe[s] / gz;
+          if (outG) outG[(int64_t)t * K + is[s]] = gj;
+          ObsFeat<R> f0, f1;
+          stat_features<R>(f0, yv0, p0[s].fam);
+          if (two) stat_features<R>(f1, yv1, p1[s].fam);
+          R accs[LOGHMM_NSLOT];
+          for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][0][qq];
+          stat_acc_rt<R>(accs, gj, p0[s], f0);
+          for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][0][qq] = accs[qq];
+          if (two) {
+            for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][1][qq];
+            stat_acc_rt<R>(accs, gj, p1[s], f1);
+            for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][1][qq] = accs[qq];
+          }
+          if (t < T - 1) gtot[s] += gj;
+          if (t == 0) g0[s] = gj;
+        }
+      }
+      if (t == 0) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          ta[is[s]] = R(0);
+          tw[is[s]] = R(0);
+        }
+        continue;
+      }
+      // xi_{t-1}: q_i = (A w_t)_i, Z = alpha~_{t-1} . q over all rows
+      R ap[2], qv[2], wj[2];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        at[s] = act[s] ? aws[(int64_t)t * K + is[s]] : R(0);
-        qe[s] = act[s] ? qws[(int64_t)t * K + is[s]] : R(0);
+        ap[s] = act[s] ? aws[(int64_t)(t - 1) * K + is[s]] : R(0);
+        wj[s] = act[s] ? wws[(int64_t)t * K + is[s]] : R(0);
+        mw[is[s]] = wj[s];
       }
-      const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
-      const R yv0 = y0g[t], yv1 = two ? y1g[t] : R(0);
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < 2; ++s) qv[s] = row_dot64<R>(As + is[s] * PITCH, mw);
+      const R Z = warp_sum(ap[0] * qv[0] + ap[1] * qv[1]);
+      const R iz = R(1) / Z;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        if (!act[s]) continue;
-        const R gj = at[s] * qe[s] / gz;
-        if (outG) outG[(int64_t)t * K + is[s]] = gj;
-        ObsFeat<R> f0, f1;
-        stat_features<R>(f0, yv0, p0[s].fam);
-        if (two) stat_features<R>(f1, yv1, p1[s].fam);
-        R accs[LOGHMM_NSLOT];
-        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][0][qq];
-        stat_acc_rt<R>(accs, gj, p0[s], f0);
-        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][0][qq] = accs[qq];
-        if (two) {
-          for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][1][qq];
-          stat_acc_rt<R>(accs, gj, p1[s], f1);
-          for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][1][qq] = accs[qq];
-        }
-        if (t < T - 1) gtot[s] += gj;
-        if (t == 0) g0[s] = gj;
+        ta[is[s]] = ap[s] * iz;
+        tw[is[s]] = wj[s];
       }
-    }
-    if (t == 0) continue;
-    // xi_{t-1}: q_i = (A w_t)_i, Z = alpha~_{t-1} . q over all rows
-    R ap[2], qv[2];
+      if (outX) {
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      ap[s] = act[s] ? aws[(int64_t)(t - 1) * K + is[s]] : R(0);
-      mw[is[s]] = act[s] ? wws[(int64_t)t * K + is[s]] : R(0);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < 2; ++s) qv[s] = row_dot64<R>(As + is[s] * PITCH, mw);
-    const R Z = warp_sum(ap[0] * qv[0] + ap[1] * qv[1]);
-    const R iz = R(1) / Z;
-    R az[RPL];
-#pragma unroll
-    for (int s = 0; s < RPL; ++s) az[s] = ap[s + h * RPL] * iz;  // h * RPL is 0 or 1
-    if constexpr (sizeof(R) == 4) {
-#pragma unroll
-      for (int c = 0; c < 64; c += 4) {
-        const float4 x = *reinterpret_cast<const float4*>(mw + c);
-#pragma unroll
-        for (int s = 0; s < RPL; ++s) {
-          X[s][c] = fma(az[s], x.x, X[s][c]);
-          X[s][c + 1] = fma(az[s], x.y, X[s][c + 1]);
-          X[s][c + 2] = fma(az[s], x.z, X[s][c + 2]);
-          X[s][c + 3] = fma(az[s], x.w, X[s][c + 3]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < 64; c += 2) {
-        const double2 x = *reinterpret_cast<const double2*>(mw + c);
-#pragma unroll
-        for (int s = 0; s < RPL; ++s) {
-          X[s][c] = fma(az[s], x.x, X[s][c]);
-          X[s][c + 1] = fma(az[s], x.y, X[s][c + 1]);
-        }
-      }
-    }
-    if (outX) {
-#pragma unroll
-      for (int s = 0; s < RPL; ++s) {
-        const int ii = is[s + h * RPL];
-        if (ii < K)
+        for (int s = 0; s < 2; ++s) {
+          if (!act[s]) continue;
           for (int jj = 0; jj < K; ++jj)
-            outX[((int64_t)(t - 1) * K + ii) * K + jj] = ap[s + h * RPL] * iz * As[ii * PITCH + jj] * mw[jj];
+            outX[((int64_t)(t - 1) * K + is[s]) * K + jj] = ap[s] * iz * As[is[s] * PITCH + jj] * mw[jj];
+        }
       }
+      __syncwarp();
     }
-    __syncwarp();
+    __syncthreads();
+    // phase 2: X[i][j] += sum_tt Ta[tt][i] Tw[tt][j]
+#pragma unroll 4
+    for (int tt = 0; tt < TC; ++tt) {
+      R av4[4], wv4[4];
+      if constexpr (sizeof(R) == 4) {
+        const float4 x = *reinterpret_cast<const float4*>(Ta + tt * 64 + 4 * ti);
+        const float4 y = *reinterpret_cast<const float4*>(Tw + tt * 64 + 4 * tj);
+        av4[0] = x.x; av4[1] = x.y; av4[2] = x.z; av4[3] = x.w;
+        wv4[0] = y.x; wv4[1] = y.y; wv4[2] = y.z; wv4[3] = y.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k += 2) {
+          const double2 x = *reinterpret_cast<const double2*>(Ta + tt * 64 + 4 * ti + k);
+          const double2 y = *reinterpret_cast<const double2*>(Tw + tt * 64 + 4 * tj + k);
+          av4[k] = x.x; av4[k + 1] = x.y;
+          wv4[k] = y.x; wv4[k + 1] = y.y;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) X[r][c] = fma(av4[r], wv4[c], X[r][c]);
+    }
+    __syncthreads();
   }
-  // fold the warps in order: xi rows, then gamma totals / first gamma / stats
+  // fold the statistics over the warps in order
   double* gts = sts + 2 * 64 * LOGHMM_NSLOT;  // [2][64]: gamma totals, first gamma
   for (int e = tid; e < 2 * 64 * LOGHMM_NSLOT + 2 * 64; e += blockDim.x) sts[e] = 0.0;
   __syncthreads();
   for (int w = 0; w < kPostWarps; ++w) {
     if (wid == w) {
-#pragma unroll
-      for (int s = 0; s < RPL; ++s) {
-        const int ii = is[s + h * RPL];
-#pragma unroll
-        for (int c = 0; c < 64; ++c) Xs[ii * 64 + c] += X[s][c];
-      }
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         for (int v = 0; v < 2; ++v)
@@ -754,19 +773,19 @@ __global__ void __launch_bounds__(256) fb_post_kernel(const FBArgs a, int K, con
     __syncthreads();
   }
   double* row = sw.seg_part + ((int64_t)b * kPostSegs + seg) * a.stats_width;
-  const int r0 = h * 32 * RPL, r1 = min(K, r0 + 32 * RPL);  // this CTA's xi rows
-  for (int e = tid; e < (r1 - r0) * K; e += blockDim.x) {
-    const int i = r0 + e / K, jj = e % K;
-    row[i * K + jj] = (double)Xs[i * 64 + jj];
-  }
-  if (do_stats) {
-    for (int jj = tid; jj < K; jj += blockDim.x) {
-      row[K * K + jj] = gts[jj];
-      row[K * K + K + jj] = gts[64 + jj];
-      for (int v = 0; v < 2; ++v)
-        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq)
-          row[K * K + 2 * K + (v * K + jj) * LOGHMM_NSLOT + qq] = sts[(v * 64 + jj) * LOGHMM_NSLOT + qq];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = 4 * ti + r, jj = 4 * tj + c;
+      if (i < K && jj < K) row[i * K + jj] = (double)X[r][c];
     }
+  for (int jj = tid; jj < K; jj += blockDim.x) {
+    row[K * K + jj] = gts[jj];
+    row[K * K + K + jj] = gts[64 + jj];
+    for (int v = 0; v < 2; ++v)
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq)
+        row[K * K + 2 * K + (v * K + jj) * LOGHMM_NSLOT + qq] = sts[(v * 64 + jj) * LOGHMM_NSLOT + qq];
   }
 }
 
