@@ -228,6 +228,18 @@ int32_t loghmm_variance_pass(int32_t dtype, loghmm_model_t* model_out, const voi
  * the first candidate that passes.  *need_more (device int) becomes nonzero if
  * a state exhausted its candidates without passing; calling again continues
  * the halving sequence (at most 60 candidates, as the reference). */
+/* Multi-rank split of loghmm_variance_pass (sequences sharded across ranks,
+ * SURVEY.md §8e): the data pass leaves this rank's per-state second-pass sums
+ * in sums[K] (fp64; only flagged states are meaningful) instead of finishing
+ * the fit; the caller all-reduces them and calls loghmm_variance_finish. */
+int32_t loghmm_variance_partial(int32_t dtype, loghmm_model_t* model_out, const void* y,
+                                const void* gamma, int64_t N, int32_t K, int32_t stream_index,
+                                const double* guard_state, double* sums, void* workspace,
+                                size_t workspace_bytes, void* stream);
+int32_t loghmm_variance_finish(loghmm_model_t* model_out, int32_t K, int32_t stream_index,
+                               const double* guard_state, const double* sums, int32_t* status,
+                               void* stream);
+
 #define LOGHMM_GUARD_CANDIDATES 8
 size_t loghmm_guard_workspace_bytes(int32_t K, int64_t N);
 int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const void* y0,
@@ -235,6 +247,19 @@ int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const voi
                              int32_t n_candidates, double* guard_state, int32_t* status,
                              int32_t* need_more, void* workspace, size_t workspace_bytes,
                              void* stream);
+
+/* Multi-rank split of loghmm_student_guard: the data pass folds this rank's
+ * sums of w*log1p(z^2/nu) into sums[K * LOGHMM_GUARD_CANDIDATES] (index
+ * j * LOGHMM_GUARD_CANDIDATES + k, k = 0 the base nu0); after the cross-rank
+ * all-reduce loghmm_student_guard_select applies the reference's acceptance
+ * rule (distributions.py:1080-1086) to the global sums. */
+int32_t loghmm_student_guard_partial(int32_t dtype, const void* y0, const void* gamma, int64_t N,
+                                     int32_t K, int32_t stream_index, int32_t n_candidates,
+                                     const double* guard_state, double* sums, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+int32_t loghmm_student_guard_select(loghmm_model_t* model_out, int32_t K, int32_t stream_index,
+                                    int32_t n_candidates, double* guard_state, const double* sums,
+                                    int32_t* status, int32_t* need_more, void* stream);
 
 #ifdef __cplusplus
 }

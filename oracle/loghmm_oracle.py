@@ -334,9 +334,18 @@ def fit(fam, y_all, w_all, ecme=(1e6, 1e-6, 50)):
                 break
         return ("von_mises", mu, k)
     if kind == "student_t":  # :1031-1087 (one ECME cycle)
+        mu, sig, nu, _ = student_t_cycle(y, w, n_tot, fam[1], fam[2], fam[3], ecme)
+        return ("student_t", mu, sig, nu)
+    raise ValueError(kind)
+
+
+def student_t_cycle(y, w, n_tot, mu0, s0, nu0, ecme=(1e6, 1e-6, 50)):
+    """One ECME cycle (distributions.py:1031-1087) on the w>0 entries; also
+    returns how many guard halvings the likelihood guard took (0 = the Newton
+    proposal passed, 60 = fell back to nu0)."""
+    if True:
         nu_ceil, nu_tol, max_newton = ecme
         n = n_tot
-        mu0, s0, nu0 = fam[1], fam[2], fam[3]
         u = (nu0 + 1.0) / (nu0 + ((y - mu0) / s0) ** 2)
         wu = w * u
         mu = float(np.dot(wu, y) / wu.sum())
@@ -368,14 +377,53 @@ def fit(fam, y_all, w_all, ecme=(1e6, 1e-6, 50)):
             if moved < nu_tol:
                 break
         base = st_ll(y, w, mu, sig, nu0)
-        for _ in range(60):
+        halvings = 60
+        for k in range(60):
             if st_ll(y, w, mu, sig, nu) >= base - 1e-12:
+                halvings = k
                 break
             nu = nu0 + 0.5 * (nu - nu0)
         else:
             nu = nu0
-        return ("student_t", mu, sig, nu)
-    raise ValueError(kind)
+        return mu, sig, nu, halvings
+
+
+# ----------------------------------------------------------------------------
+# exhaustive path enumeration (the reference's tests/oracles.py:281-350 used by
+# test_acceptance.py:70-91 and test_inference.py): tiny K, T only
+# ----------------------------------------------------------------------------
+
+
+def enumerate_paths(log_pi, log_a, log_b):
+    """Joint log-probability of every state path, lexicographic order."""
+    import itertools
+
+    T, K = log_b.shape
+    out = []
+    for path in itertools.product(range(K), repeat=T):
+        lp = log_pi[path[0]] + log_b[0, path[0]]
+        for t in range(1, T):
+            lp += log_a[path[t - 1], path[t]] + log_b[t, path[t]]
+        out.append((path, float(lp)))
+    return out
+
+
+def brute_force(log_pi, log_a, log_b):
+    """(log-likelihood, gamma [T, K], best path, best joint) by enumeration;
+    the best path is the first (lexicographically smallest) maximiser."""
+    paths = enumerate_paths(log_pi, log_a, log_b)
+    lps = np.array([lp for _, lp in paths])
+    mx = lps.max()
+    ll = float(mx + math.log(np.exp(lps - mx).sum())) if np.isfinite(mx) else -math.inf
+    T, K = log_b.shape
+    g = np.zeros((T, K))
+    for (path, lp) in paths:
+        if np.isfinite(lp):
+            w = math.exp(lp - ll)
+            for t, s in enumerate(path):
+                g[t, s] += w
+    best = int(np.argmax(lps))
+    return ll, g, tuple(paths[best][0]), float(lps[best])
 
 
 # ----------------------------------------------------------------------------

@@ -102,6 +102,11 @@ _SIGNATURES = {
         _i32,
         [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp],
     ),
+    "loghmm_variance_partial": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "loghmm_variance_finish": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "loghmm_student_guard_partial": (
+        _i32, [_i32, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "loghmm_student_guard_select": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

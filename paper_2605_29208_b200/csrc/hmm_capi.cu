@@ -548,8 +548,7 @@ int32_t loghmm_reduce_stats(const double* partials, const double* ll, int64_t B,
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 
-// per-block partial sums of the guard / variance passes; the pass counter
-// (zero-initialised workspace, reset by the last block) follows them
+// per-block partial sums of the guard / variance passes (after the counter)
 static inline size_t kGuardPartBytes(int K) {
   return (size_t)148 * 4 * K * LOGHMM_GUARD_CANDIDATES * sizeof(double);
 }
@@ -577,9 +576,16 @@ int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64
 
 static constexpr int kReduceBlocks = 256;  // upper bound on the reduction grid
 
+// Workspace layouts of the passes that keep an inter-block counter: the
+// counter lives in the first 256 bytes (a K- and width-independent place, so
+// a workspace reused by calls of different shapes always finds it at zero:
+// the buffer is zero-filled once and the last block of every launch resets
+// it), the block partials follow at offset kCounterBytes.
+static constexpr size_t kCounterBytes = 256;
+
 size_t loghmm_reduce_workspace_bytes(int64_t B, int64_t width) {
   (void)B;
-  return align256((size_t)kReduceBlocks * (size_t)(width + 1) * sizeof(double)) + 256;
+  return kCounterBytes + align256((size_t)kReduceBlocks * (size_t)(width + 1) * sizeof(double));
 }
 
 int32_t loghmm_reduce_mstep(const double* partials, const double* ll, int64_t B, int64_t width,
@@ -593,9 +599,8 @@ int32_t loghmm_reduce_mstep(const double* partials, const double* ll, int64_t B,
   if (do_mstep && (!model_out || !status || !guard_state || n_sequences < 1)) return LOGHMM_EINVAL;
   if (!workspace || workspace_bytes < loghmm_reduce_workspace_bytes(B, width))
     return LOGHMM_EWORKSPACE;
-  double* part = (double*)workspace;
-  unsigned* counter =
-      (unsigned*)((char*)workspace + align256((size_t)kReduceBlocks * (size_t)(width + 1) * 8));
+  unsigned* counter = (unsigned*)workspace;
+  double* part = (double*)((char*)workspace + kCounterBytes);
   // totals + one row of column sums per thread group (see the kernel)
   // 1024 threads = G row groups x (width + 1) columns; about sqrt(B) blocks so
   // that both reduction levels keep ~B / (G * sqrt(B)) rows per thread (one
@@ -619,44 +624,72 @@ int32_t loghmm_reduce_mstep(const double* partials, const double* ll, int64_t B,
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 
+static int32_t variance_launch(int32_t dtype, loghmm_model_t* model_out, const void* y,
+                               const void* gamma, int64_t N, int32_t K, int32_t stream_index,
+                               const double* guard_state, int32_t* status, double* sums,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  if (!model_out || !y || !gamma || !guard_state || K < 1 || K > LOGHMM_MAX_STATES) return LOGHMM_EINVAL;
+  if (workspace_bytes < loghmm_guard_workspace_bytes(K, N)) return LOGHMM_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nblocks = 148 * 2;
+  unsigned* counter = (unsigned*)workspace;
+  double* part = (double*)((char*)workspace + kCounterBytes);
+  if (dtype == LOGHMM_F64)
+    variance_pass_kernel<double><<<nblocks, 256, 0, st>>>((const double*)y, (const double*)gamma, N,
+                                                          K, stream_index, model_out, guard_state,
+                                                          part, counter, status, sums);
+  else
+    variance_pass_kernel<float><<<nblocks, 256, 0, st>>>((const float*)y, (const float*)gamma, N, K,
+                                                         stream_index, model_out, guard_state,
+                                                         part, counter, status, sums);
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
 int32_t loghmm_variance_pass(int32_t dtype, loghmm_model_t* model_out, const void* y,
                              const void* gamma, int64_t N, int32_t K, int32_t stream_index,
                              const double* guard_state, int32_t* status, void* workspace,
                              size_t workspace_bytes, void* stream) {
-  if (!model_out || !y || !gamma || !guard_state || !status || K < 1) return LOGHMM_EINVAL;
-  if (workspace_bytes < loghmm_guard_workspace_bytes(K, N)) return LOGHMM_EWORKSPACE;
-  cudaStream_t st = (cudaStream_t)stream;
-  const int nblocks = 148 * 2;
-  double* part = (double*)workspace;
-  unsigned* counter = (unsigned*)((char*)workspace + kGuardPartBytes(K));
-  if (dtype == LOGHMM_F64)
-    variance_pass_kernel<double><<<nblocks, 256, 0, st>>>((const double*)y, (const double*)gamma, N,
-                                                          K, stream_index, model_out, guard_state,
-                                                          part, counter, status);
-  else
-    variance_pass_kernel<float><<<nblocks, 256, 0, st>>>((const float*)y, (const float*)gamma, N, K,
-                                                         stream_index, model_out, guard_state,
-                                                         part, counter, status);
+  if (!status) return LOGHMM_EINVAL;
+  return variance_launch(dtype, model_out, y, gamma, N, K, stream_index, guard_state, status, nullptr,
+                         workspace, workspace_bytes, stream);
+}
+
+int32_t loghmm_variance_partial(int32_t dtype, loghmm_model_t* model_out, const void* y,
+                                const void* gamma, int64_t N, int32_t K, int32_t stream_index,
+                                const double* guard_state, double* sums, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  if (!sums) return LOGHMM_EINVAL;
+  return variance_launch(dtype, model_out, y, gamma, N, K, stream_index, guard_state, nullptr, sums,
+                         workspace, workspace_bytes, stream);
+}
+
+int32_t loghmm_variance_finish(loghmm_model_t* model_out, int32_t K, int32_t stream_index,
+                               const double* guard_state, const double* sums, int32_t* status,
+                               void* stream) {
+  if (!model_out || !guard_state || !sums || !status || K < 1 || K > LOGHMM_MAX_STATES)
+    return LOGHMM_EINVAL;
+  variance_finish_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(model_out, K, stream_index, guard_state,
+                                                             sums, status);
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 
 size_t loghmm_guard_workspace_bytes(int32_t K, int64_t N) {
   (void)N;
-  return align256(kGuardPartBytes(K) + 16);
+  return kCounterBytes + align256(kGuardPartBytes(K));
 }
 
-int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const void* y0,
-                             const void* gamma, int64_t N, int32_t K, int32_t stream_index,
-                             int32_t n_candidates, double* guard_state, int32_t* status,
-                             int32_t* need_more, void* workspace, size_t workspace_bytes,
-                             void* stream) {
-  if (!model_out || !y0 || !gamma || !guard_state || !status || !need_more || K < 1 ||
-      n_candidates < 2 || n_candidates > LOGHMM_GUARD_CANDIDATES)
+static int32_t guard_launch(int32_t dtype, loghmm_model_t* model_out, const void* y0,
+                            const void* gamma, int64_t N, int32_t K, int32_t stream_index,
+                            int32_t n_candidates, double* guard_state, int32_t* status,
+                            int32_t* need_more, double* sums, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  if (!y0 || !gamma || !guard_state || K < 1 || K > LOGHMM_MAX_STATES || n_candidates < 2 ||
+      n_candidates > LOGHMM_GUARD_CANDIDATES)
     return LOGHMM_EINVAL;
   if (workspace_bytes < loghmm_guard_workspace_bytes(K, N)) return LOGHMM_EWORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   const int nblocks = 148 * 4;
-  double* part = (double*)workspace;
+  double* part = (double*)((char*)workspace + kCounterBytes);  // (counter area left untouched)
   if (dtype == LOGHMM_F64)
     student_guard_kernel<double><<<nblocks, 256, 0, st>>>((const double*)y0, (const double*)gamma,
                                                           N, K, stream_index, guard_state,
@@ -665,8 +698,43 @@ int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const voi
     student_guard_kernel<float><<<nblocks, 256, 0, st>>>((const float*)y0, (const float*)gamma, N,
                                                          K, stream_index, guard_state,
                                                          n_candidates, part);
-  guard_select_kernel<<<1, 64, 0, st>>>(model_out, K, stream_index, guard_state, n_candidates,
-                                        part, nblocks, status, need_more);
+  if (sums) {
+    guard_fold_kernel<<<1, 64, 0, st>>>(K, stream_index, guard_state, n_candidates, part, nblocks, sums);
+  } else {
+    guard_select_kernel<<<1, 64, 0, st>>>(model_out, K, stream_index, guard_state, n_candidates,
+                                          part, nblocks, status, need_more);
+  }
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
+int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const void* y0,
+                             const void* gamma, int64_t N, int32_t K, int32_t stream_index,
+                             int32_t n_candidates, double* guard_state, int32_t* status,
+                             int32_t* need_more, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  if (!model_out || !status || !need_more) return LOGHMM_EINVAL;
+  return guard_launch(dtype, model_out, y0, gamma, N, K, stream_index, n_candidates, guard_state,
+                      status, need_more, nullptr, workspace, workspace_bytes, stream);
+}
+
+int32_t loghmm_student_guard_partial(int32_t dtype, const void* y0, const void* gamma, int64_t N,
+                                     int32_t K, int32_t stream_index, int32_t n_candidates,
+                                     const double* guard_state, double* sums, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+  if (!sums) return LOGHMM_EINVAL;
+  return guard_launch(dtype, nullptr, y0, gamma, N, K, stream_index, n_candidates,
+                      const_cast<double*>(guard_state), nullptr, nullptr, sums, workspace,
+                      workspace_bytes, stream);
+}
+
+int32_t loghmm_student_guard_select(loghmm_model_t* model_out, int32_t K, int32_t stream_index,
+                                    int32_t n_candidates, double* guard_state, const double* sums,
+                                    int32_t* status, int32_t* need_more, void* stream) {
+  if (!model_out || !guard_state || !sums || !status || !need_more || K < 1 ||
+      K > LOGHMM_MAX_STATES || n_candidates < 2 || n_candidates > LOGHMM_GUARD_CANDIDATES)
+    return LOGHMM_EINVAL;
+  guard_select_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(model_out, K, stream_index, guard_state,
+                                                          n_candidates, sums, 1, status, need_more);
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }
 

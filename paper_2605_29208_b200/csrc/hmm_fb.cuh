@@ -176,16 +176,37 @@ __device__ __forceinline__ void flush_slab(R* __restrict__ out, const R* __restr
 }
 
 // Matrix product Z = X * Y (K x K), FMA.
+// sum_i a_i b_i over the K states, in index order.  For K = 2 the two
+// products are rounded separately and added (no contraction), so relabelling
+// the two states permutes the result bit for bit -- the exact label-swap
+// equivariance the reference's numpy arithmetic has (test_training.py:177-197).
+template <typename R, int K, typename F>
+__device__ __forceinline__ R sdot(F ab) {
+  if constexpr (K == 2) {
+    R a0, b0, a1, b1;
+    ab(0, a0, b0);
+    ab(1, a1, b1);
+    return Num<R>::add(Num<R>::mul(a0, b0), Num<R>::mul(a1, b1));
+  } else {
+    R a, b;
+    ab(0, a, b);
+    R acc = a * b;
+#pragma unroll
+    for (int i = 1; i < K; ++i) {
+      ab(i, a, b);
+      acc = fma(a, b, acc);
+    }
+    return acc;
+  }
+}
+
 template <typename R, int K>
 __device__ __forceinline__ void matmul(const R (&X)[K][K], const R (&Y)[K][K], R (&Z)[K][K]) {
 #pragma unroll
   for (int r = 0; r < K; ++r)
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      R acc = X[r][0] * Y[0][c];
-#pragma unroll
-      for (int i = 1; i < K; ++i) acc = fma(X[r][i], Y[i][c], acc);
-      Z[r][c] = acc;
+      Z[r][c] = sdot<R, K>([&](int i, R& a, R& b) { a = X[r][i]; b = Y[i][c]; });
     }
 }
 
@@ -272,6 +293,29 @@ __device__ __forceinline__ void shfl_mat(R (&Z)[K][K], double& off, const R (&X)
 // ---------------------------------------------------------------------------
 // Emission evaluation for all states at one step (fast contract).
 // ---------------------------------------------------------------------------
+// Column-scaled transition matrix for the linear scaled recursions:
+// Ahat_ij = A_ij / c_j with c_j = max_i A_ij, and lc_j = log(c_j) in the
+// requested base (-inf for an all-zero column, whose Ahat column is zero).
+// The emission shift of every step is then max_j (log b_j + lc_j) instead of
+// max_j log b_j, i.e. it follows the best state that can be ENTERED: a
+// structurally unreachable state with an overwhelming emission no longer
+// pushes the reachable terms below the floating-point range (the failure the
+// log-space reference never has, inference.py:129-146).  b_j A_ij is
+// unchanged: 2^(u_j + lc_j - m) Ahat_ij = 2^(u_j - m) A_ij.
+template <typename R, int K>
+__device__ __forceinline__ void load_colscaled(const loghmm_model_t* __restrict__ md, R (&Am)[K][K],
+                                               R (&lc)[K], double base_log2) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double c = 0.0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) c = fmax(c, md->A[i * K + j]);
+    lc[j] = c > 0.0 ? (R)(log2(c) * base_log2) : Num<R>::ninf();
+#pragma unroll
+    for (int i = 0; i < K; ++i) Am[i][j] = c > 0.0 ? (R)(md->A[i * K + j] / c) : R(0);
+  }
+}
+
 template <typename R, int K, int CFG>
 struct Emit {
   EmP<R> e0[K];
@@ -466,15 +510,13 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
 
   // ---- model -------------------------------------------------------------
   const loghmm_model_t* __restrict__ md = a.model;
-  R Am[K][K];
+  R Am[K][K], lcn[K];  // column-scaled A and log c_j (natural log)
+  load_colscaled<R, K>(md, Am, lcn, 0.6931471805599453094);
   R minA = R(1);
 #pragma unroll
   for (int i = 0; i < K; ++i)
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      Am[i][j] = (R)md->A[i * K + j];
-      minA = Am[i][j] < minA ? Am[i][j] : minA;
-    }
+    for (int j = 0; j < K; ++j) minA = Am[i][j] < minA ? Am[i][j] : minA;
   R lpi[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) lpi[j] = (R)md->log_pi[j];
@@ -565,6 +607,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
         for (int j = 0; j < K; ++j) seed_u[j] = (lpi[j] + lb[j]) * kL2E;
         continue;
       }
+      // shift by the best enterable state (load_colscaled)
+#pragma unroll
+      for (int j = 0; j < K; ++j) lb[j] += lcn[j];
+      m = lb[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) m = rmax(m, lb[j]);
       const bool finite_m = m > N::ninf();
       const R m2 = m * kL2E;
       R bt[K];
@@ -575,9 +623,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
       for (int r = 0; r < K; ++r)
 #pragma unroll
         for (int c = 0; c < K; ++c) {
-          R acc = Mop[r][0] * Am[0][c];
-#pragma unroll
-          for (int i = 1; i < K; ++i) acc = fma(Mop[r][i], Am[i][c], acc);
+          const R acc = sdot<R, K>([&](int i, R& a, R& b) { a = Mop[r][i]; b = Am[i][c]; });
           Nw[r][c] = acc * bt[c];
         }
 #pragma unroll
@@ -635,10 +681,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
     R v[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      R acc = sv[0] * Q[0][c];
-#pragma unroll
-      for (int i = 1; i < K; ++i) acc = fma(sv[i], Q[i][c], acc);
-      v[c] = acc;
+      v[c] = sdot<R, K>([&](int i, R& a, R& b) { a = sv[i]; b = Q[i][c]; });
     }
     double vo = so + qo;
     normalise_vec2<R, K>(v, vo);
@@ -739,6 +782,8 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
         ObsFeat<R> f0, f1;
         R lb[K];
         em.eval(yat0(s + 1), yat1(s + 1), f0, f1, lb, oob);
+#pragma unroll
+        for (int j = 0; j < K; ++j) lb[j] += lcn[j];  // (load_colscaled)
         R m = lb[0];
 #pragma unroll
         for (int j = 1; j < K; ++j) m = rmax(m, lb[j]);
@@ -750,9 +795,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
         R q[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-          R acc = Am[i][0] * w[0];
-#pragma unroll
-          for (int j = 1; j < K; ++j) acc = fma(Am[i][j], w[j], acc);
+          R acc = sdot<R, K>([&](int j, R& a, R& b) { a = Am[i][j]; b = w[j]; });
           q[i] = acc;
         }
         rho += fin ? (double)m2 : 0.0;
@@ -863,6 +906,8 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
 #pragma unroll
           for (int j = 0; j < K; ++j) g0[j] = g[j];
         } else {
+#pragma unroll
+          for (int j = 0; j < K; ++j) lb[j] += lcn[j];  // (load_colscaled)
           R m = lb[0];
 #pragma unroll
           for (int j = 1; j < K; ++j) m = rmax(m, lb[j]);
@@ -873,9 +918,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
           for (int j = 0; j < K; ++j) bb[j] = fin ? N::fex2(fma(lb[j], kL2E, -m2)) : R(0);
 #pragma unroll
           for (int c = 0; c < K; ++c) {
-            R acc = av[0] * Am[0][c];
-#pragma unroll
-            for (int i = 1; i < K; ++i) acc = fma(av[i], Am[i][c], acc);
+            R acc = sdot<R, K>([&](int i, R& a, R& b) { a = av[i]; b = Am[i][c]; });
             p[c] = acc;
           }
           if (outA) {
@@ -887,12 +930,9 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 2) fb_small_kernel(c
           }
           // pair (t-1, t): xi_{t-1}(i,j) = a_{t-1}[i] A_ij bb_j beta~_t[j] / Z
           R v[K];
-          R Z = R(0);
 #pragma unroll
-          for (int j = 0; j < K; ++j) {
-            v[j] = bb[j] * bet[j];
-            Z = fma(p[j], v[j], Z);
-          }
+          for (int j = 0; j < K; ++j) v[j] = bb[j] * bet[j];
+          const R Z = sdot<R, K>([&](int j, R& a, R& b) { a = p[j]; b = v[j]; });
           const R iz = N::frcp(Z);
           R cv[K];
 #pragma unroll

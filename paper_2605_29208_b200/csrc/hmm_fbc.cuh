@@ -280,13 +280,20 @@ struct V {
 
 // Emission log2-densities of all states (u_j = log2 b_j(y)).  The Gaussian is
 // rewritten as u = c - w^2 with w = y*s - mu*s, s = sqrt(log2(e)/2)/sigma.
+// eval() returns v_j = u_j + lc_j, the log2-density plus the log2 column
+// scale of the column-scaled transition matrix (load_colscaled): the
+// recursions shift by max_j v_j and multiply by Ahat.  eval_raw() returns
+// u_j itself (t = 0, where pi rather than A leads into the state, and the
+// dead-step rescan).
 template <typename R, int K, int CFG>
 struct Em2 {
   Emit<R, K, CFG> em;
-  R ga[K], go[K], gc[K];
+  R ga[K], go[K], gc[K], lc[K];
   __device__ __forceinline__ void load(const loghmm_model_t* m, int n_streams, int fams,
-                                       const double* lut, int lut_n) {
+                                       const double* lut, int lut_n, const R (&lc2)[K]) {
     em.load(m, n_streams, fams, lut, lut_n);
+#pragma unroll
+    for (int j = 0; j < K; ++j) lc[j] = lc2[j];
     if constexpr (CFG == kCfgGauss) {
       const double h = sqrt(0.5 * 1.4426950408889634);
 #pragma unroll
@@ -294,7 +301,7 @@ struct Em2 {
         const double s = h / m->em[0][j].p[1];
         ga[j] = (R)s;
         go[j] = (R)(-m->em[0][j].p[0] * s);
-        gc[j] = (R)(m->em[0][j].c[0] * 1.4426950408889634);
+        gc[j] = (R)(m->em[0][j].c[0] * 1.4426950408889634) + lc2[j];
       }
     }
   }
@@ -310,8 +317,15 @@ struct Em2 {
       R lb[K];
       em.eval(y0, y1, f0, f1, lb, oob);
 #pragma unroll
-      for (int j = 0; j < K; ++j) u[j] = lb[j] * R(1.4426950408889634);
+      for (int j = 0; j < K; ++j) u[j] = fma(lb[j], R(1.4426950408889634), lc[j]);
     }
+  }
+  __device__ __forceinline__ void eval_raw(R y0, R y1, R (&u)[K], bool& oob) const {
+    ObsFeat<R> f0, f1;
+    R lb[K];
+    em.eval(y0, y1, f0, f1, lb, oob);
+#pragma unroll
+    for (int j = 0; j < K; ++j) u[j] = lb[j] * R(1.4426950408889634);
   }
 };
 
@@ -479,20 +493,18 @@ __global__ void __launch_bounds__(128)
 
     // ---- model -----------------------------------------------------------
     const loghmm_model_t* __restrict__ md = a.model;
-    R Am[K][K];
+    R Am[K][K], lc2[K];  // column-scaled A (load_colscaled), log2 c_j
+    load_colscaled<R, K>(md, Am, lc2, 1.0);
     R minA = R(1);
 #pragma unroll
     for (int i = 0; i < K; ++i)
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        Am[i][j] = (R)md->A[i * K + j];
-        minA = fmin(Am[i][j], minA);
-      }
+      for (int j = 0; j < K; ++j) minA = fmin(Am[i][j], minA);
     R lpi2[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) lpi2[j] = (R)(md->log_pi[j] * 1.4426950408889634);
     Em2<R, K, CFG> em;
-    em.load(md, a.n_streams, a.stream_fams, a.lut, a.lut_n);
+    em.load(md, a.n_streams, a.stream_fams, a.lut, a.lut_n, lc2);
     // Pass-1 operator renormalisation every nn steps: its max entry shrinks
     // by at most min(A) per step, so nn steps stay above 2^-100 (fp32) /
     // 2^-900 (fp64).  (Pass 2 renormalises every step through the emission
@@ -566,8 +578,12 @@ __global__ void __launch_bounds__(128)
             // t = 0 (lane 0, first group) seeds the forward vector
             // (log2 pi + log2 b_0): no operator step
             const bool first = (g == 0) && (lane == 0);
+            if (first) {
+              R ur[K];
+              em.eval_raw(yv0, yv1, ur, oob);
 #pragma unroll
-            for (int j = 0; j < K; ++j) seed_u[j] = first ? lpi2[j] + u[j] : seed_u[j];
+              for (int j = 0; j < K; ++j) seed_u[j] = lpi2[j] + ur[j];
+            }
 #pragma unroll
             for (int r = 0; r < K; ++r)
 #pragma unroll
@@ -893,7 +909,22 @@ __global__ void __launch_bounds__(128)
           }
           V<R, K>::mul(av, p, bh);
           lam += m;
-          if constexpr (!PH2) park_st(i, av);
+          if constexpr (!PH2) {
+            if (sub == 0 && g == 0 && lane == 0) {
+              // t = 0: alpha_0 = pi b_0 in log2 form, exactly (pi, not A,
+              // leads into the states, so the column scale does not apply)
+              R ur[K], o[K];
+              em.eval_raw(yf.v[0], two ? yf1.v[0] : R(0), ur, oob);
+              V<R, K>::add(ur, ur, lpi2);
+              const R m0 = fmax(V<R, K>::vmax(ur), kFloor);
+#pragma unroll
+              for (int j = 0; j < K; ++j) av[j] = N::fex2(ur[j] - m0);
+              lam = m0;
+              V<R, K>::mul_s(o, kLN2, ur);
+              SVec<R, K>::st(myA, o);
+            }
+            park_st(i, av);
+          }
         }
         // ------------- backward step: y index r = t + 1 = L-1-i -------------
         {
@@ -997,9 +1028,8 @@ __global__ void __launch_bounds__(128)
           const R yv0 = y0c[s];
           const R yv1 = two ? y1c[s] : R(0);
           if (yv0 != yv0 || yv1 != yv1) nan_seen = true;
-          ObsFeat<R> f0, f1;
           R u[K];
-          em.eval(yv0, yv1, f0, f1, u, oob);
+          em.eval_raw(yv0, yv1, u, oob);
           R m = u[0];
 #pragma unroll
           for (int j = 1; j < K; ++j) m = fmax(m, u[j]);

@@ -845,8 +845,9 @@ __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int
   const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
   const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
   uint8_t* bk = backws + start * K;
-  bool oob = false;
+  bool oob = false, nan_seen = false;
   auto logb = [&](R v0, R v1) -> R {
+    nan_seen |= (v0 != v0) | (v1 != v1);  // inference.py:117-118 (validate_sequence)
     R v = exact_logb<R>(e0, v0, a.lut, a.lut_n, oob);
     if (two) v = N::add(v, exact_logb<R>(e1, v1, a.lut, a.lut_n, oob));
     return v;
@@ -906,6 +907,7 @@ __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int
         bi = i;
       }
     a.log_joint[b] = (double)bv;
+    if (a.flags && (nan_seen || oob)) a.flags[2 * b + 1] |= (nan_seen ? 1 : 0) | (oob ? 2 : 0);
     s_cur = bi;
   }
   __syncthreads();

@@ -679,7 +679,8 @@ __global__ void __launch_bounds__(256) variance_pass_kernel(const R* __restrict_
                                                             const double* __restrict__ guard,
                                                             double* __restrict__ part,
                                                             unsigned* __restrict__ counter,
-                                                            int32_t* __restrict__ status) {
+                                                            int32_t* __restrict__ status,
+                                                            double* __restrict__ sums_out) {
   __shared__ double red[256];
   __shared__ bool last;
   __shared__ unsigned flagged;
@@ -730,9 +731,38 @@ __global__ void __launch_bounds__(256) variance_pass_kernel(const R* __restrict_
   if (j < K && guard[(size_t)(sidx * K + j) * kGuardStride + 8] != 0.0) {
     double S = 0.0;
     for (unsigned blk = 0; blk < gridDim.x; ++blk) S += __ldcg(part + (size_t)blk * K + j);
-    variance_finish_state(mout, K, sidx, j, guard, S, status);
+    // multi-rank split: leave this rank's sum for the cross-rank all-reduce
+    if (sums_out) sums_out[j] = S;
+    else variance_finish_state(mout, K, sidx, j, guard, S, status);
   }
   if (threadIdx.x == 0) *counter = 0u;
+}
+
+// Finish of the multi-rank split: sums[j] is the all-reduced second-pass sum.
+__global__ void variance_finish_kernel(loghmm_model_t* __restrict__ mout, int K, int sidx,
+                                       const double* __restrict__ guard,
+                                       const double* __restrict__ sums,
+                                       int32_t* __restrict__ status) {
+  const int j = threadIdx.x;
+  if (j < K && guard[(size_t)(sidx * K + j) * kGuardStride + 8] != 0.0)
+    variance_finish_state(mout, K, sidx, j, guard, sums[j], status);
+}
+
+// Block partials of the guard pass folded in block order into
+// sums[j * LOGHMM_GUARD_CANDIDATES + k] (pending states only; zeros else), the
+// per-rank input of the cross-rank all-reduce.
+__global__ void guard_fold_kernel(int K, int sidx, const double* __restrict__ guard, int ncand,
+                                  const double* __restrict__ part, int nblocks,
+                                  double* __restrict__ sums) {
+  const int j = threadIdx.x;
+  if (j >= K) return;
+  const bool pending = guard[(size_t)(sidx * K + j) * kGuardStride + 5] != 0.0;
+  for (int k = 0; k < LOGHMM_GUARD_CANDIDATES; ++k) {
+    double acc = 0.0;
+    if (pending && k < ncand)
+      for (int blk = 0; blk < nblocks; ++blk) acc += part[((size_t)blk * K + j) * LOGHMM_GUARD_CANDIDATES + k];
+    sums[(size_t)j * LOGHMM_GUARD_CANDIDATES + k] = acc;
+  }
 }
 
 }  // namespace lhmm

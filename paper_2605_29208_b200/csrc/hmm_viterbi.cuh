@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
   ExactEm<R, VF::F1> em1;
   if (two) em1.load(md->em[1][jj]);
   else em1.fam = LOGHMM_FAM_NONE;
-  bool oob = false;
+  bool oob = false, nan_seen = false;
   const double* lut = a.lut;
   const int lut_n = a.lut_n;
 
@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
   }
   __syncwarp();
 
-  auto emis = [&](R yv0, R yv1) -> R {
+  // ok: the step exists (the ring also feeds steps past the sequence end)
+  auto emis = [&](R yv0, R yv1, bool ok) -> R {
+    nan_seen |= ok & ((yv0 != yv0) | (yv1 != yv1));  // inference.py:117-118
     R lb = em0.eval(yv0, lut, lut_n, oob);
     if (two) lb = N::add(lb, em1.eval(yv1, lut, lut_n, oob));
     return lb;
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
 
   // ---- forward max-plus recursion ---------------------------------------
   R delta = N::ninf();
-  if (T > 0) delta = N::add((R)md->log_pi[jj], emis(y0g[0], two ? y1g[0] : R(0)));
+  if (T > 0) delta = N::add((R)md->log_pi[jj], emis(y0g[0], two ? y1g[0] : R(0), true));
 
   // One recursion step.  Every lane executes it (no divergence around the
   // shuffles / ballots); lanes past their sequence end keep their score.  The
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
     const R* r0 = ring_at(0, 0, g);
     const R* r1 = ring_at(0, NS - 1, g);
 #pragma unroll
-    for (int u = 0; u < H; ++u) lbs[u] = emis(r0[u], two ? r1[u] : R(0));
+    for (int u = 0; u < H; ++u) lbs[u] = emis(r0[u], two ? r1[u] : R(0), 1 + u < T);
   }
 #pragma unroll 1
   for (int c = 0; c < nchunks; ++c) {
@@ -287,27 +289,27 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
     if (t + 32 <= Tmin) {  // every sequence of the warp covers the chunk
 #pragma unroll
       for (int u = 0; u < H; ++u) {
-        lbn[u] = emis(r0[H + u], two ? r1[H + u] : R(0));
+        lbn[u] = emis(r0[H + u], two ? r1[H + u] : R(0), t + H + u < T);
         step(t + u, lbs[u], true);
       }
       cp_async_wait<1>();
       __syncwarp();
 #pragma unroll
       for (int u = 0; u < H; ++u) {
-        lbs[u] = emis(n0[u], two ? n1[u] : R(0));
+        lbs[u] = emis(n0[u], two ? n1[u] : R(0), t + 32 + u < T);
         step(t + H + u, lbn[u], true);
       }
     } else {
 #pragma unroll
       for (int u = 0; u < H; ++u) {
-        lbn[u] = emis(r0[H + u], two ? r1[H + u] : R(0));
+        lbn[u] = emis(r0[H + u], two ? r1[H + u] : R(0), t + H + u < T);
         step(t + u, lbs[u], t + u < T);
       }
       cp_async_wait<1>();
       __syncwarp();
 #pragma unroll
       for (int u = 0; u < H; ++u) {
-        lbs[u] = emis(n0[u], two ? n1[u] : R(0));
+        lbs[u] = emis(n0[u], two ? n1[u] : R(0), t + 32 + u < T);
         step(t + H + u, lbn[u], t + H + u < T);
       }
     }
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(128) viterbi_small_kernel(const VitArgs a) {
   }
   if (valid && j == 0) {
     a.log_joint[b] = (double)best_val;
-    if (a.flags && oob) a.flags[2 * b + 1] |= 2;
+    if (a.flags && (oob || nan_seen)) a.flags[2 * b + 1] |= (oob ? 2 : 0) | (nan_seen ? 1 : 0);
   }
 
   // ---- backtrace: the K lanes of group g walk K segments of its sequence --

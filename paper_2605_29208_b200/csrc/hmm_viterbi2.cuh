@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
     if (two) em1[l].load(md->em[1][js]);
     else em1[l].fam = LOGHMM_FAM_NONE;
   }
-  bool oob = false;
+  bool oob = false, nan_seen = false;
   const double* lut = a.lut;
   const int lut_n = a.lut_n;
 
@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
   const int Tlast = T > 0 ? T - 1 : 0;
 
   auto emis = [&](int l, R yv0, R yv1) -> R {
+    nan_seen |= (yv0 != yv0) | (yv1 != yv1);  // inference.py:117-118
     R lb = em0[l].eval(yv0, lut, lut_n, oob);
     if (two) lb = N::add(lb, em1[l].eval(yv1, lut, lut_n, oob));
     return padj[l] ? N::ninf() : lb;
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(128) viterbi2_kernel(const VitArgs a) {
   }
   if (valid && h == 0) {
     a.log_joint[b] = (double)best_val;
-    if (a.flags && oob) a.flags[2 * b + 1] |= 2;
+    if (a.flags && (oob || nan_seen)) a.flags[2 * b + 1] |= (oob ? 2 : 0) | (nan_seen ? 1 : 0);
   }
   __syncwarp();
 

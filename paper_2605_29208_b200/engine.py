@@ -432,3 +432,51 @@ def student_guard(batch: Batch, dm_out: DeviceModel, gamma: torch.Tensor, stream
                                _ptr(need_more), wptr, wlen, _stream()),
         "loghmm_student_guard",
     )
+
+
+def variance_partial(batch: Batch, dm_out: DeviceModel, gamma: torch.Tensor, stream_index: int,
+                     guard: torch.Tensor, sums: torch.Tensor) -> None:
+    """Multi-rank split of variance_pass: this rank's second-pass sums -> sums[K]."""
+    L = lib()
+    K = dm_out.K
+    y = batch.y0 if stream_index == 0 else batch.y1
+    wptr, wlen = _WS_GUARD.get(int(L.loghmm_guard_workspace_bytes(K, batch.N)), y.device)
+    check(L.loghmm_variance_partial(_code(batch.dtype), dm_out.ptr(), _ptr(y), _ptr(gamma), batch.N,
+                                    K, stream_index, _ptr(guard), _ptr(sums), wptr, wlen, _stream()),
+          "loghmm_variance_partial")
+
+
+def variance_finish(dm_out: DeviceModel, stream_index: int, guard: torch.Tensor,
+                    sums: torch.Tensor, status: torch.Tensor) -> None:
+    check(lib().loghmm_variance_finish(dm_out.ptr(), dm_out.K, stream_index, _ptr(guard), _ptr(sums),
+                                       _ptr(status), _stream()), "loghmm_variance_finish")
+
+
+def student_guard_partial(batch: Batch, dm_out: DeviceModel, gamma: torch.Tensor,
+                          stream_index: int, n_candidates: int, guard: torch.Tensor,
+                          sums: torch.Tensor) -> None:
+    """Multi-rank split of student_guard: this rank's candidate sums ->
+    sums[K * GUARD_CANDIDATES]."""
+    L = lib()
+    K = dm_out.K
+    y = batch.y0 if stream_index == 0 else batch.y1
+    wptr, wlen = _WS_GUARD.get(int(L.loghmm_guard_workspace_bytes(K, batch.N)), y.device)
+    check(L.loghmm_student_guard_partial(_code(batch.dtype), _ptr(y), _ptr(gamma), batch.N, K,
+                                         stream_index, n_candidates, _ptr(guard), _ptr(sums), wptr,
+                                         wlen, _stream()), "loghmm_student_guard_partial")
+
+
+def student_guard_select(dm_out: DeviceModel, stream_index: int, n_candidates: int,
+                         guard: torch.Tensor, sums: torch.Tensor, status: torch.Tensor,
+                         need_more: torch.Tensor) -> None:
+    check(lib().loghmm_student_guard_select(dm_out.ptr(), dm_out.K, stream_index, n_candidates,
+                                            _ptr(guard), _ptr(sums), _ptr(status), _ptr(need_more),
+                                            _stream()), "loghmm_student_guard_select")
+
+
+# Candidate batches of the ECME guard: the first launch evaluates the base and
+# GUARD_CANDIDATES-1 halvings, each further launch the next GUARD_CANDIDATES-1;
+# the reference tries at most 60 halvings (distributions.py:1083), so this
+# many launches always reach a decision (a launch with nothing pending exits
+# at once).  Used where the host cannot poll need_more (CUDA graph capture).
+GUARD_LAUNCHES = -(-60 // (_native.GUARD_CANDIDATES - 1))

@@ -182,6 +182,10 @@ def _np(t):
 def emission_log_matrix(model: HmmModel, sequence, dtype="float64"):
     """T x K matrix of per-state emission log-densities (inference.py:122-126)."""
     dm, batch = _single(model, sequence, dtype)
+    # validate_sequence (inference.py:113-119): the NaN check the reference
+    # runs before evaluating any density
+    if bool(torch.isnan(batch.y0).any()) or (batch.y1 is not None and bool(torch.isnan(batch.y1).any())):
+        raise ValueError("observation sequence contains NaN")
     out = engine.emission(batch, dm)
     return out.cpu().numpy() if not torch.is_tensor(sequence) else out
 
@@ -241,6 +245,7 @@ def viterbi(model: HmmModel, sequence, dtype="float64"):
     dm, batch = _single(model, sequence, dtype)
     o = engine.viterbi(batch, dm)
     lj = o.log_joint.cpu().numpy()
+    _raise_flags(o.flags.cpu().numpy(), None, None)  # NaN (validate_sequence) first
     if lj[0] == -np.inf:
         raise InfeasibleSequenceError("no feasible path")
     return ViterbiResult(path=o.path.cpu().numpy(), log_joint=float(lj[0]))
@@ -272,6 +277,8 @@ def viterbi_batch(model: HmmModel, data, dtype="float64", *, back=False,
     dm = engine.DeviceModel.from_model(model)
     batch = engine.make_batch(data, model.n_streams, dtype)
     o = engine.viterbi(batch, dm, back=back)
+    if check:
+        _raise_flags(o.flags.cpu().numpy(), None, None)
     if check and (o.log_joint.cpu().numpy() == -np.inf).any():
         raise InfeasibleSequenceError("no feasible path")
     return BatchViterbi(o.path, o.log_joint, batch.offsets_host, o.back)

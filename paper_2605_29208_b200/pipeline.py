@@ -25,7 +25,7 @@ import torch
 
 from . import _native, engine
 from .inference import HmmModel
-from .training import TrainingConfig, model_from_record
+from .training import TrainingConfig, apply_mstep_status, model_from_record
 
 __all__ = ["Pipeline"]
 
@@ -72,6 +72,9 @@ class Pipeline:
         self.status = torch.zeros(self.ns * K, dtype=torch.int32, device=dev)
         self.guard = torch.zeros(self.ns * K * engine.GUARD_STRIDE, dtype=torch.float64, device=dev)
         self.need_more = torch.zeros(1, dtype=torch.int32, device=dev)
+        # per-rank second-pass sums (multi-rank split only)
+        self.var_sums = torch.zeros(K, dtype=torch.float64, device=dev)
+        self.guard_sums = torch.zeros(K * _native.GUARD_CANDIDATES, dtype=torch.float64, device=dev)
         self.ws_fb = engine.Workspace()
         self.ws_vit = engine.Workspace()
         self.ws_red = engine.Workspace()
@@ -91,8 +94,10 @@ class Pipeline:
 
     @property
     def kernels_per_run(self) -> int:
-        # + one variance pass per variance stream, + guard & select per Student-t stream
-        return self.KERNELS_PER_RUN + len(self.var_streams) + 2 * len(self.student_streams)
+        # + one variance pass per variance stream, + guard & select launches
+        # per Student-t stream
+        return (self.KERNELS_PER_RUN + len(self.var_streams)
+                + 2 * engine.GUARD_LAUNCHES * len(self.student_streams))
 
     def load(self, y) -> None:
         """Copy observations [B, T] (or [B, T, 2]) into the device batch."""
@@ -153,17 +158,53 @@ class Pipeline:
                                 self.config, self.dm_next, self.status, self.guard, self.td,
                                 workspace=self.ws_red)
         else:
-            import torch.distributed as dist
-
             engine.reduce_mstep(self.fb.partials, self.fb.ll, self.totals, workspace=self.ws_red)
-            dist.all_reduce(self.totals, group=self.pg)
+            self._all_reduce(self.totals)
             engine.mstep(self.dm, self.totals, self.B * self._world(), self.config, self.dm_next,
                          self.status, self.guard, self.td)
+        # exact second passes (two-pass variance, ECME likelihood guard); with
+        # a process group their data sums are all-reduced before the finish,
+        # exactly like the statistics vector (sequences are sharded)
         for s in self.var_streams:
-            engine.variance_pass(self.batch, self.dm_next, self.fb.gamma, s, self.guard, self.status)
+            if self.pg is None:
+                engine.variance_pass(self.batch, self.dm_next, self.fb.gamma, s, self.guard,
+                                     self.status)
+            else:
+                engine.variance_partial(self.batch, self.dm_next, self.fb.gamma, s, self.guard,
+                                        self.var_sums)
+                self._all_reduce(self.var_sums)
+                engine.variance_finish(self.dm_next, s, self.guard, self.var_sums, self.status)
+        # ECME guard (distributions.py:1080-1086): the full halving sequence,
+        # in fixed candidate batches so the step needs no host round trip (a
+        # batch with no pending state exits at once); training.baum_welch polls
+        # need_more instead, with identical results
         for s in self.student_streams:
-            engine.student_guard(self.batch, self.dm_next, self.fb.gamma, s, 2, self.guard,
-                                 self.status, self.need_more)
+            for _ in range(engine.GUARD_LAUNCHES):
+                if self.pg is None:
+                    engine.student_guard(self.batch, self.dm_next, self.fb.gamma, s,
+                                         _native.GUARD_CANDIDATES, self.guard, self.status,
+                                         self.need_more)
+                else:
+                    engine.student_guard_partial(self.batch, self.dm_next, self.fb.gamma, s,
+                                                 _native.GUARD_CANDIDATES, self.guard,
+                                                 self.guard_sums)
+                    self._all_reduce(self.guard_sums)
+                    engine.student_guard_select(self.dm_next, s, _native.GUARD_CANDIDATES,
+                                                self.guard, self.guard_sums, self.status,
+                                                self.need_more)
+
+    def _all_reduce(self, t: torch.Tensor) -> None:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, group=self.pg)
+
+    def check(self) -> list[int]:
+        """Host read of the step's per-state M-step status: raises
+        TrainingError / warns FitWarning exactly as baum_welch does
+        (training.py:130-148) and returns the collapsed states."""
+        fams = [[int(self.dm.host["em"][s, j]["family"]) for j in range(self.K)]
+                for s in range(self.ns)]
+        return apply_mstep_status(self.status.cpu().numpy(), fams)
 
     def _slice_plan(self, n: int):
         """Per-slice views (batch, FB outputs, Viterbi outputs) of n equal

@@ -126,12 +126,40 @@ def _warn_texts(fam: str, st: int) -> list[str]:
     return out
 
 
-def model_from_record(rec: np.ndarray) -> HmmModel:
-    """HmmModel from a device loghmm_model_t read back to the host."""
+def apply_mstep_status(st: np.ndarray, fams, stacklevel: int = 2) -> list[int]:
+    """Raise / warn for the per-state M-step status words the way
+    m_step_emissions and the family fits do (training.py:130-148,
+    distributions.py FitWarning sites); returns the collapsed states.
+
+    ``fams[s][j]`` is the family code of state j in stream s."""
+    ns = len(fams)
+    K = len(fams[0])
+    collapsed = []
+    for j in range(K):
+        for s in range(ns):
+            code = int(st[s * K + j])
+            fam = _FAM_NAME[fams[s][j]]
+            base = code & 0xFF
+            if base >= 16:
+                raise TrainingError(f"state {j}: {_ERR_TEXT[base](fam)}")
+            for msg in _warn_texts(fam, code):
+                warnings.warn(msg, FitWarning, stacklevel=stacklevel)
+        if int(st[j]) & 0xFF == _native.MS_COLLAPSED:
+            collapsed.append(j)
+    return collapsed
+
+
+def model_from_record(rec: np.ndarray, keep=None) -> HmmModel:
+    """HmmModel from a device loghmm_model_t read back to the host.  States
+    whose ``keep[j]`` is not None return that object (collapsed states keep
+    their distribution object, training.py:139-141)."""
     K = int(rec["K"])
     ns = int(rec["n_streams"])
     ems = []
     for j in range(K):
+        if keep is not None and keep[j] is not None:
+            ems.append(keep[j])
+            continue
         parts = [from_record(int(rec["em"][s, j]["family"]), rec["em"][s, j]["p"]) for s in range(ns)]
         ems.append(parts[0] if ns == 1 else Joint(parts[0], parts[1]))
     pi = np.array(rec["pi"][:K], dtype=float)
@@ -159,6 +187,8 @@ def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtyp
     """EM training: returns the refined model and the per-iteration trace."""
     config = config or TrainingConfig()
     ns = model.n_streams
+    if isinstance(data, (list, tuple)) and len(data) == 0:
+        raise TrainingError("training data contains no sequences")  # training.py:151-156
     batch = engine.make_batch(data, ns, dtype)
     K = model.num_states
     dm_cur = engine.DeviceModel.from_model(model)
@@ -182,6 +212,7 @@ def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtyp
     collapsed_states: list[tuple[int, int]] = []
     converged = False
     n_msteps = 0
+    kept = list(model.emissions)  # objects untouched by every M-step so far
     for iteration in range(1, config.max_iterations + 1):
         if iteration > 1:
             engine.forward_backward(batch, dm_cur, alpha=False, beta=False, gamma=need_gamma,
@@ -210,22 +241,17 @@ def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtyp
                 if int(need_more.item()) == 0:
                     break
                 ncand = _native.GUARD_CANDIDATES
-        st = status.cpu().numpy()
+        collapsed = apply_mstep_status(status.cpu().numpy(), fams, stacklevel=3)
+        collapsed_states.extend((iteration, j) for j in collapsed)
+        # a collapsed state keeps its distribution object (m_step_emissions
+        # returns ``dist`` itself, training.py:139-141)
         for j in range(K):
-            for s in range(ns):
-                code = int(st[s * K + j])
-                fam = _FAM_NAME[fams[s][j]]
-                base = code & 0xFF
-                if base >= 16:
-                    raise TrainingError(f"state {j}: {_ERR_TEXT[base](fam)}")
-                for msg in _warn_texts(fam, code):
-                    warnings.warn(msg, FitWarning, stacklevel=2)
-            if int(st[j]) & 0xFF == _native.MS_COLLAPSED:
-                collapsed_states.append((iteration, j))
+            if j not in collapsed:
+                kept[j] = None
         dm_cur, dm_next = dm_next, dm_cur
         n_msteps += 1
 
-    current = model if n_msteps == 0 else model_from_record(dm_cur.to_host())
+    current = model if n_msteps == 0 else model_from_record(dm_cur.to_host(), keep=kept)
     report = TrainingReport(
         log_likelihood_trace=trace,
         iterations=len(trace),
