@@ -302,17 +302,29 @@ __device__ __forceinline__ void shfl_mat(R (&Z)[K][K], double& off, const R (&X)
 // pushes the reachable terms below the floating-point range (the failure the
 // log-space reference never has, inference.py:129-146).  b_j A_ij is
 // unchanged: 2^(u_j + lc_j - m) Ahat_ij = 2^(u_j - m) A_ij.
+// Every warp runs this prologue for its own sequence, so it is kept cheap:
+// one reciprocal and one log per column, in the recursion's precision (an
+// error of a few ulps in the scale multiplies a whole column of b_j A_ij by
+// the same factor 1 + O(eps_R): far inside the posterior tolerances).
 template <typename R, int K>
 __device__ __forceinline__ void load_colscaled(const loghmm_model_t* __restrict__ md, R (&Am)[K][K],
                                                R (&lc)[K], double base_log2) {
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    double c = 0.0;
+    R c = R(0);
 #pragma unroll
-    for (int i = 0; i < K; ++i) c = fmax(c, md->A[i * K + j]);
-    lc[j] = c > 0.0 ? (R)(log2(c) * base_log2) : Num<R>::ninf();
+    for (int i = 0; i < K; ++i) {
+      Am[i][j] = (R)md->A[i * K + j];
+      c = c > Am[i][j] ? c : Am[i][j];
+    }
+    const bool nz = c > R(0);
+    const R rc = nz ? Num<R>::frcp(c) : R(0);
+    if constexpr (sizeof(R) == 4)
+      lc[j] = nz ? Num<R>::flg2(c) * (R)base_log2 : Num<R>::ninf();
+    else
+      lc[j] = nz ? log2(c) * base_log2 : Num<R>::ninf();
 #pragma unroll
-    for (int i = 0; i < K; ++i) Am[i][j] = c > 0.0 ? (R)(md->A[i * K + j] / c) : R(0);
+    for (int i = 0; i < K; ++i) Am[i][j] *= rc;
   }
 }
 

@@ -543,9 +543,22 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
       for (int c = 0; c < K; ++c) Mop[r][c] = r == c ? R(1) : R(0);
     R moff = R(0);
-    R seed_u[K];
+    // lane 0's t = 0 seed log2(pi) + log2 b_0 with the raw densities (pi,
+    // not A, leads into the states), evaluated once outside the loops; the
+    // pass-2 forward start alpha~_0 follows from it
+    R seed_u[K], av0[K], out0[K], m0;
+    {
+      R ur[K];
+      em.eval_raw(y0c[0], two ? y1c[0] : R(0), ur, oob);
 #pragma unroll
-    for (int j = 0; j < K; ++j) seed_u[j] = N::ninf();
+      for (int j = 0; j < K; ++j) seed_u[j] = lane == 0 ? lpi2[j] + ur[j] : N::ninf();
+      m0 = fmax(V<R, K>::vmax(seed_u), kFloor);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        av0[j] = N::fex2(seed_u[j] - m0);
+        out0[j] = seed_u[j] * kLN2;
+      }
+    }
     {
       Y4<R> yc, yc1, yn, yn1;
       yc.load(y0c);
@@ -578,12 +591,6 @@ __global__ void __launch_bounds__(128)
             // t = 0 (lane 0, first group) seeds the forward vector
             // (log2 pi + log2 b_0): no operator step
             const bool first = (g == 0) && (lane == 0);
-            if (first) {
-              R ur[K];
-              em.eval_raw(yv0, yv1, ur, oob);
-#pragma unroll
-              for (int j = 0; j < K; ++j) seed_u[j] = lpi2[j] + ur[j];
-            }
 #pragma unroll
             for (int r = 0; r < K; ++r)
 #pragma unroll
@@ -837,8 +844,9 @@ __global__ void __launch_bounds__(128)
     // One 4-step group of both directions.  PH2: second half (meet).  The
     // carried vectors are renormalised every step through the emission shift:
     // scaling by 2^-log2(max v) keeps max v in [min(A)^2 / 2, 2].
-    auto group = [&](int g, auto ph2c) {
+    auto group = [&](int g, auto ph2c, auto firstc) {
       constexpr bool PH2 = decltype(ph2c)::value;
+      constexpr bool FIRST = decltype(firstc)::value;  // g == 0 (peeled)
       Y4<R> yfn, yfn1, ybn, ybn1;
       if (g + 1 < NG) {
         yfn.load(y0c + 4 * (g + 1));
@@ -881,18 +889,17 @@ __global__ void __launch_bounds__(128)
           V<R, K>::mul_s(p, av[0], Am[0]);
 #pragma unroll
           for (int r = 1; r < K; ++r) V<R, K>::fma_s(p, av[r], Am[r], p);
-          if (!PH2 && sub == 0) {
-            if (g == 0 && lane == 0) {  // t = 0: p = pi (linear), offset 0
-#pragma unroll
-              for (int j = 0; j < K; ++j) p[j] = (R)__ldg(&md->pi[j]);
-            }
-          }
+          const bool t0 = FIRST && sub == 0 && lane == 0;  // alpha_0 = pi b_0 exactly
           {
             R o[K], l2[K];
 #pragma unroll
             for (int j = 0; j < K; ++j) l2[j] = N::flg2(p[j]);
             V<R, K>::add(l2, l2, u);
             V<R, K>::fma_ss(o, kLN2, l2, lam * kLN2);
+            if constexpr (FIRST) {
+#pragma unroll
+              for (int j = 0; j < K; ++j) o[j] = t0 ? out0[j] : o[j];
+            }
             SVec<R, K>::st(myA + sub * K, o);
           }
           if constexpr (PH2) {
@@ -909,22 +916,12 @@ __global__ void __launch_bounds__(128)
           }
           V<R, K>::mul(av, p, bh);
           lam += m;
-          if constexpr (!PH2) {
-            if (sub == 0 && g == 0 && lane == 0) {
-              // t = 0: alpha_0 = pi b_0 in log2 form, exactly (pi, not A,
-              // leads into the states, so the column scale does not apply)
-              R ur[K], o[K];
-              em.eval_raw(yf.v[0], two ? yf1.v[0] : R(0), ur, oob);
-              V<R, K>::add(ur, ur, lpi2);
-              const R m0 = fmax(V<R, K>::vmax(ur), kFloor);
+          if constexpr (FIRST) {
 #pragma unroll
-              for (int j = 0; j < K; ++j) av[j] = N::fex2(ur[j] - m0);
-              lam = m0;
-              V<R, K>::mul_s(o, kLN2, ur);
-              SVec<R, K>::st(myA, o);
-            }
-            park_st(i, av);
+            for (int j = 0; j < K; ++j) av[j] = t0 ? av0[j] : av[j];
+            lam = t0 ? m0 : lam;
           }
+          if constexpr (!PH2) park_st(i, av);
         }
         // ------------- backward step: y index r = t + 1 = L-1-i -------------
         {
@@ -984,8 +981,9 @@ __global__ void __launch_bounds__(128)
       }
     };
 
+    group(0, std::false_type{}, std::true_type{});
 #pragma unroll 1
-    for (int g = 0; g < NG / 2; ++g) group(g, std::false_type{});
+    for (int g = 1; g < NG / 2; ++g) group(g, std::false_type{}, std::false_type{});
     {
       // boundary: gamma_{HL-1} from alpha~_{HL-1} (av) and beta~_{HL-1} (bt);
       // it is the first pending posterior of the backward direction
@@ -997,7 +995,7 @@ __global__ void __launch_bounds__(128)
       __syncwarp();
     }
 #pragma unroll 1
-    for (int g = NG / 2; g < NG; ++g) group(g, std::true_type{});
+    for (int g = NG / 2; g < NG; ++g) group(g, std::true_type{}, std::false_type{});
     if constexpr (CFG == kCfgGauss) {
 #pragma unroll
       for (int j = 0; j < K; ++j) {
