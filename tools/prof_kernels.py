@@ -53,6 +53,16 @@ def main():
         out["fb_ms"] = timeit(lambda: engine.forward_backward(batch, dm, stats=True, out=fbo), a.reps, flush)
         out["fb_nostats_noout_ms"] = timeit(
             lambda: engine.forward_backward(batch, dm, alpha=False, beta=False, gamma=False), a.reps, flush)
+    if a.only in ("", "fb", "fbm") and hasattr(engine.lib(), "loghmm_fb_mstep"):
+        from paper_2605_29208_b200.training import TrainingConfig
+        tc = TrainingConfig()
+        tot = torch.empty(fbo.partials.shape[1] + 1, dtype=torch.float64, device="cuda")
+        dm2 = engine.DeviceModel.from_model(cfg.init)
+        st = torch.zeros(2 * dm.K, dtype=torch.int32, device="cuda")
+        gd = torch.zeros(2 * dm.K * engine.GUARD_STRIDE, dtype=torch.float64, device="cuda")
+        ws = engine.Workspace()
+        out["fb_mstep_ms"] = timeit(lambda: engine.fb_mstep(batch, dm, fbo, tot, tc, dm2, st, gd, ws),
+                                    a.reps, flush)
     if a.only in ("", "vit"):
         out["vit_ms"] = timeit(lambda: engine.viterbi(batch, dm, out=vo), a.reps, flush)
     if a.only in ("", "small"):
