@@ -63,7 +63,19 @@ enum loghmm_family {
   LOGHMM_FAM_STUDENT_T = 2, /* p = {mu, sigma, nu}        distributions.py:512-537 */
   LOGHMM_FAM_GAMMA = 3,     /* p = {shape, rate}          distributions.py:366-389 */
   LOGHMM_FAM_VON_MISES = 4, /* p = {mu, kappa}            distributions.py:343-363 */
-  LOGHMM_FAM_POISSON = 5    /* p = {lambda}               distributions.py:246-263 */
+  LOGHMM_FAM_POISSON = 5,   /* p = {lambda}               distributions.py:246-263 */
+  /* off the benchmarked configurations (runtime-family kernel paths; fits by
+   * loghmm_ext_fit_pass); record layouts in distributions.py record() */
+  LOGHMM_FAM_LOGNORMAL = 6,   /* p = {mu, sigma}     c = {log sigma, 0.5 LOG_2PI}      :208-227 */
+  LOGHMM_FAM_EXPONENTIAL = 7, /* p = {lambda}        c = {log lambda}                  :230-244 */
+  LOGHMM_FAM_RAYLEIGH = 8,    /* p = {sigma}         c = {log s2, 2 s2}                :267-283 */
+  LOGHMM_FAM_UNIFORM = 9,     /* p = {a, b}          c = {-log(b - a)}                 :286-305 */
+  LOGHMM_FAM_CATEGORICAL = 10,/* p, c = log p_0..7, reserved = category count (<= 8)   :308-341 */
+  LOGHMM_FAM_BETA = 11,       /* p = {alpha, beta}   c = {log B(alpha, beta)}          :393-413 */
+  LOGHMM_FAM_WEIBULL = 12,    /* p = {k, lambda}     c = {log k - log lambda}          :416-439 */
+  LOGHMM_FAM_NEGBINOM = 13,   /* p = {r, p}          c = {lgamma r, r log p, log1p(-p)} :442-469 */
+  LOGHMM_FAM_CHISQ = 14,      /* p = {nu}            c = {h log 2, lgamma h, h - 1}    :472-489 */
+  LOGHMM_FAM_PARETO = 15      /* p = {xm, alpha}     c = {log a + a log xm, a + 1}     :492-510 */
 };
 
 /* Return codes. */
@@ -183,10 +195,14 @@ enum loghmm_mstep_status {
   LOGHMM_MS_ERR_GAMMA_VAR = 18,      /* "gamma fit is degenerate: weighted variance is zero" */
   LOGHMM_MS_ERR_GAMMA_GAP = 19,      /* "gamma fit is degenerate: zero log-moment gap" */
   LOGHMM_MS_ERR_NONFINITE = 20,      /* von_mises non-finite angles */
+  LOGHMM_MS_ERR_DEGENERATE = 21,     /* exponential / weibull / negative_binomial / pareto degenerate fit */
+  LOGHMM_MS_ERR_CAT_CODE = 22,       /* "categorical fit saw code >= m" */
   LOGHMM_MS_WARN_NEWTON = 1 << 8,    /* FitWarning: Newton did not converge */
   LOGHMM_MS_WARN_CEILING = 1 << 9,   /* FitWarning: ceiling clamp */
-  LOGHMM_MS_WARN_BOUNDARY = 1 << 10, /* FitWarning: von Mises resultant at boundary */
-  LOGHMM_MS_STUDENT_GUARD = 1 << 12  /* Student-t state awaiting the LL guard */
+  LOGHMM_MS_WARN_BOUNDARY = 1 << 10, /* FitWarning: von Mises resultant at boundary / NegBin underdispersed */
+  LOGHMM_MS_WARN_ITERCAP = 1 << 11,  /* FitWarning: beta fit hit the iteration cap */
+  LOGHMM_MS_STUDENT_GUARD = 1 << 12, /* Student-t state awaiting the LL guard */
+  LOGHMM_MS_EXT_FIT = 1 << 13        /* state of families 6..15 awaiting loghmm_ext_fit_pass */
 };
 int32_t loghmm_mstep(const loghmm_model_t* model_in, const double* totals, int64_t n_sequences,
                      double collapse_epsilon, double nu_ceiling, double nu_tol, int32_t max_newton,
@@ -247,6 +263,24 @@ int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const voi
                              int32_t n_candidates, double* guard_state, int32_t* status,
                              int32_t* need_more, void* workspace, size_t workspace_bytes,
                              void* stream);
+
+/* Weighted-sample M-step fits of the families LOGHMM_FAM_LOGNORMAL ..
+ * LOGHMM_FAM_PARETO (distributions.py:639-723 closed forms, :789-871 Beta and
+ * Weibull, :919-973 NegativeBinomial and ChiSquared) for the states
+ * loghmm_mstep left pending (status bit LOGHMM_MS_EXT_FIT).  One call = one
+ * data pass over y and gamma[:, j] of every pending state of the stream plus
+ * a per-state finish step that advances its program (moments -> centred
+ * moments -> Newton iterations); *need_more (device int, zeroed by the
+ * caller) becomes nonzero while some state needs another pass.  Fits end by
+ * writing the parameters and density constants into model_out; failures set
+ * the LOGHMM_MS_ERR_* status codes, FitWarnings the LOGHMM_MS_WARN_* bits.
+ * At most LOGHMM_EXT_MAX_PASSES calls are needed.  Workspace:
+ * loghmm_guard_workspace_bytes. */
+#define LOGHMM_EXT_MAX_PASSES 64
+int32_t loghmm_ext_fit_pass(int32_t dtype, loghmm_model_t* model_out, const void* y, const void* gamma,
+                            int64_t N, int32_t K, int32_t stream_index, double* guard_state,
+                            int32_t* status, int32_t* need_more, void* workspace,
+                            size_t workspace_bytes, void* stream);
 
 /* Multi-rank split of loghmm_student_guard: the data pass folds this rank's
  * sums of w*log1p(z^2/nu) into sums[K * LOGHMM_GUARD_CANDIDATES] (index

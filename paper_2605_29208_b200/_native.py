@@ -35,7 +35,10 @@ MAX_STREAMS = 2
 NSLOT = 6
 GUARD_CANDIDATES = 8
 F32, F64 = 0, 1
-FAM = {"none": 0, "gaussian": 1, "student_t": 2, "gamma": 3, "von_mises": 4, "poisson": 5}
+FAM = {"none": 0, "gaussian": 1, "student_t": 2, "gamma": 3, "von_mises": 4, "poisson": 5,
+       "lognormal": 6, "exponential": 7, "rayleigh": 8, "uniform": 9, "categorical": 10, "beta": 11,
+       "weibull": 12, "negative_binomial": 13, "chi_squared": 14, "pareto": 15}
+EXT_FAMILIES = frozenset(n for n, v in FAM.items() if v >= 6)  # fitted by csrc/hmm_extfit.cuh
 
 # Mirrors loghmm_emission_t / loghmm_model_t (natural alignment, no padding).
 EMISSION_DTYPE = np.dtype(
@@ -62,10 +65,15 @@ MS_ERR_SUPPORT = 17
 MS_ERR_GAMMA_VAR = 18
 MS_ERR_GAMMA_GAP = 19
 MS_ERR_NONFINITE = 20
+MS_ERR_DEGENERATE = 21
+MS_ERR_CAT_CODE = 22
 MS_WARN_NEWTON = 1 << 8
 MS_WARN_CEILING = 1 << 9
 MS_WARN_BOUNDARY = 1 << 10
+MS_WARN_ITERCAP = 1 << 11
 MS_STUDENT_GUARD = 1 << 12
+MS_EXT_FIT = 1 << 13
+EXT_MAX_PASSES = 64
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -102,6 +110,7 @@ _SIGNATURES = {
         _i32,
         [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp],
     ),
+    "loghmm_ext_fit_pass": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "loghmm_variance_partial": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
     "loghmm_variance_finish": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "loghmm_student_guard_partial": (

@@ -717,6 +717,27 @@ int32_t loghmm_student_guard(int32_t dtype, loghmm_model_t* model_out, const voi
                       status, need_more, nullptr, workspace, workspace_bytes, stream);
 }
 
+int32_t loghmm_ext_fit_pass(int32_t dtype, loghmm_model_t* model_out, const void* y, const void* gamma,
+                            int64_t N, int32_t K, int32_t stream_index, double* guard_state,
+                            int32_t* status, int32_t* need_more, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  if (!model_out || !y || !gamma || !guard_state || !status || !need_more || K < 1 ||
+      K > LOGHMM_MAX_STATES)
+    return LOGHMM_EINVAL;
+  if (!workspace || workspace_bytes < loghmm_guard_workspace_bytes(K, N)) return LOGHMM_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = (double*)((char*)workspace + kCounterBytes);
+  if (dtype == LOGHMM_F64)
+    ext_pass_kernel<double><<<kExtBlocks, 256, 0, st>>>((const double*)y, (const double*)gamma, N, K,
+                                                        stream_index, model_out, guard_state, status, part);
+  else
+    ext_pass_kernel<float><<<kExtBlocks, 256, 0, st>>>((const float*)y, (const float*)gamma, N, K,
+                                                       stream_index, model_out, guard_state, status, part);
+  ext_finish_kernel<<<1, 64, 0, st>>>(model_out, K, stream_index, guard_state, status, part, kExtBlocks,
+                                      need_more);
+  return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
+}
+
 int32_t loghmm_student_guard_partial(int32_t dtype, const void* y0, const void* gamma, int64_t N,
                                      int32_t K, int32_t stream_index, int32_t n_candidates,
                                      const double* guard_state, double* sums, void* workspace,

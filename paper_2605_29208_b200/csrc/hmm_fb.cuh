@@ -437,7 +437,10 @@ __device__ __forceinline__ void stat_acc_rt(R (&acc)[LOGHMM_NSLOT], R w, const E
     case LOGHMM_FAM_GAMMA: stat_acc<R, LOGHMM_FAM_GAMMA>(acc, w, p, f); break;
     case LOGHMM_FAM_VON_MISES: stat_acc<R, LOGHMM_FAM_VON_MISES>(acc, w, p, f); break;
     case LOGHMM_FAM_POISSON: stat_acc<R, LOGHMM_FAM_POISSON>(acc, w, p, f); break;
-    default: break;
+    case LOGHMM_FAM_NONE: break;
+    // families 6..15: only the state's total weight (the collapse guard,
+    // training.py:139); their fits run weighted-sample passes (hmm_extfit.cuh)
+    default: acc[0] += w; break;
   }
 }
 

@@ -90,6 +90,7 @@ __device__ inline double sp_i1_i0_ratio(double k) {
 constexpr double kLog2Pi = 1.8378770664093453;  // math.log(2*pi)
 constexpr double kScaleFloor = 1e-9;             // distributions.py:73
 constexpr double kKappaCeiling = 1e5;            // distributions.py:74
+constexpr double kNegbinomCeiling = 1e6;         // distributions.py:76
 
 // Host-equivalent constants of a record (see loghmm_emission_t).
 __device__ inline void em_constants(loghmm_emission_t& e) {
@@ -430,6 +431,12 @@ __device__ void mstep_body(const loghmm_model_t* __restrict__ min_, const double
           break;
         }
         default:
+          // families 6..15: fitted by the weighted-sample passes
+          // (hmm_extfit.cuh, loghmm_ext_fit_pass) after this kernel
+          if (e.family >= LOGHMM_FAM_LOGNORMAL) {
+            st |= LOGHMM_MS_EXT_FIT;
+            gs[0] = 0.0;
+          }
           break;
       }
     }
@@ -766,3 +773,5 @@ __global__ void guard_fold_kernel(int K, int sidx, const double* __restrict__ gu
 }
 
 }  // namespace lhmm
+
+#include "hmm_extfit.cuh"

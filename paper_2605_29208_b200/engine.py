@@ -128,6 +128,8 @@ def make_batch(data, n_streams: int = 1, dtype="float64", device=None) -> Batch:
         B, T = int(arr.shape[0]), int(arr.shape[1])
         if T < 1 or B < 1:
             raise ValueError(_SEQ_ERR)
+        if isinstance(arr, np.ndarray):
+            arr = np.ascontiguousarray(arr)  # (reversed / strided views)
         t = torch.as_tensor(arr)
         t = t.to(device=dev, dtype=td, non_blocking=True)
         if n_streams == 1:
@@ -179,7 +181,9 @@ def encode_model(model) -> np.ndarray:
     for j, e in enumerate(ems):
         parts = (e.first, e.second) if n_streams == 2 else (e,)
         for s, d in enumerate(parts):
-            fam, p, c = d.record()
+            r = d.record()
+            fam, p, c = r[:3]
+            rec["em"][s, j]["reserved"] = r[3] if len(r) > 3 else 0  # categorical: category count
             rec["em"][s, j]["family"] = fam
             rec["em"][s, j]["p"] = p
             rec["em"][s, j]["c"] = c
@@ -480,3 +484,24 @@ def student_guard_select(dm_out: DeviceModel, stream_index: int, n_candidates: i
 # many launches always reach a decision (a launch with nothing pending exits
 # at once).  Used where the host cannot poll need_more (CUDA graph capture).
 GUARD_LAUNCHES = -(-60 // (_native.GUARD_CANDIDATES - 1))
+
+
+def ext_fit(batch: Batch, dm_out: DeviceModel, gamma: torch.Tensor, stream_index: int,
+            guard: torch.Tensor, status: torch.Tensor, need_more: torch.Tensor,
+            poll: bool = True) -> None:
+    """Weighted-sample fits of the families 6..15 left pending by the M-step
+    (loghmm_ext_fit_pass, one data pass per call).  poll=True reads need_more
+    after each pass (host loop); poll=False enqueues the maximum number of
+    passes (a pass with nothing pending exits at once; CUDA-graph safe)."""
+    L = lib()
+    K = dm_out.K
+    y = batch.y0 if stream_index == 0 else batch.y1
+    wptr, wlen = _WS_GUARD.get(int(L.loghmm_guard_workspace_bytes(K, batch.N)), y.device)
+    for _ in range(_native.EXT_MAX_PASSES):
+        if poll:
+            need_more.zero_()
+        check(L.loghmm_ext_fit_pass(_code(batch.dtype), dm_out.ptr(), _ptr(y), _ptr(gamma), batch.N, K,
+                                    stream_index, _ptr(guard), _ptr(status), _ptr(need_more), wptr,
+                                    wlen, _stream()), "loghmm_ext_fit_pass")
+        if poll and int(need_more.item()) == 0:
+            break

@@ -86,6 +86,10 @@ class Pipeline:
         var_fams = (_native.FAM["gaussian"], _native.FAM["gamma"], _native.FAM["student_t"])
         self.var_streams = [s for s in range(self.ns)
                             if any(int(fams[s, j]) in var_fams for j in range(K))]
+        self.ext_streams = [s for s in range(self.ns)
+                            if any(int(fams[s, j]) >= _native.FAM["lognormal"] for j in range(K))]
+        if self.ext_streams and process_group is not None:
+            raise NotImplementedError("multi-rank steps support the five hot-path families only")
         self.s_copy = torch.cuda.Stream(device=dev)
         self._slices = {}
         # per-kernel CUDA events (recorded on the stream each kernel runs on)
@@ -97,7 +101,8 @@ class Pipeline:
         # + one variance pass per variance stream, + guard & select launches
         # per Student-t stream
         return (self.KERNELS_PER_RUN + len(self.var_streams)
-                + 2 * engine.GUARD_LAUNCHES * len(self.student_streams))
+                + 2 * engine.GUARD_LAUNCHES * len(self.student_streams)
+                + 2 * _native.EXT_MAX_PASSES * len(self.ext_streams))
 
     def load(self, y) -> None:
         """Copy observations [B, T] (or [B, T, 2]) into the device batch."""
@@ -192,6 +197,12 @@ class Pipeline:
                     engine.student_guard_select(self.dm_next, s, _native.GUARD_CANDIDATES,
                                                 self.guard, self.guard_sums, self.status,
                                                 self.need_more)
+
+        # families 6..15: the weighted-sample fit passes (fixed count; a pass
+        # with nothing pending exits at once)
+        for s in self.ext_streams:
+            engine.ext_fit(self.batch, self.dm_next, self.fb.gamma, s, self.guard, self.status,
+                           self.need_more, poll=False)
 
     def _all_reduce(self, t: torch.Tensor) -> None:
         import torch.distributed as dist

@@ -98,12 +98,30 @@ def count_parameters(model: HmmModel) -> int:
 
 _FAM_NAME = {v: k for k, v in _native.FAM.items()}
 
+_SUPPORT_TEXT = {  # distributions.py:623-629 _validate_support and the per-fit checks
+    "poisson": "poisson fit requires non-negative integer observations",
+    "gamma": "gamma fit requires strictly positive observations",
+    "lognormal": "lognormal fit requires strictly positive observations",
+    "exponential": "exponential fit requires non-negative observations",
+    "rayleigh": "rayleigh fit requires non-negative observations",
+    "categorical": "categorical fit requires non-negative integer observations",
+    "beta": "beta fit requires observations strictly inside (0, 1)",
+    "weibull": "weibull fit requires strictly positive observations",
+    "negative_binomial": "negative_binomial fit requires non-negative integer observations",
+    "chi_squared": "chi_squared fit requires strictly positive observations",
+    "pareto": "pareto fit requires strictly positive observations",
+}
+_DEGENERATE_TEXT = {
+    "exponential": "exponential fit is degenerate: weighted mean is zero",
+    "weibull": "weibull fit is degenerate: weighted variance is zero",
+    "negative_binomial": "negative_binomial fit is degenerate: all observations are zero",
+    "pareto": "pareto fit is degenerate: all weighted observations equal the minimum",
+}
+
 _ERR_TEXT = {
     _native.MS_ERR_NO_MASS: lambda fam: "fit requires positive total weight",
-    _native.MS_ERR_SUPPORT: lambda fam: {
-        "poisson": "poisson fit requires non-negative integer observations",
-        "gamma": "gamma fit requires strictly positive observations",
-    }.get(fam, f"{fam} fit support violation"),
+    _native.MS_ERR_SUPPORT: lambda fam: _SUPPORT_TEXT.get(fam, f"{fam} fit support violation"),
+    _native.MS_ERR_DEGENERATE: lambda fam: _DEGENERATE_TEXT.get(fam, f"{fam} fit is degenerate"),
     _native.MS_ERR_GAMMA_VAR: lambda fam: "gamma fit is degenerate: weighted variance is zero",
     _native.MS_ERR_GAMMA_GAP: lambda fam: "gamma fit is degenerate: zero log-moment gap",
     _native.MS_ERR_NONFINITE: lambda fam: "von_mises fit requires finite angles",
@@ -123,10 +141,32 @@ def _warn_texts(fam: str, st: int) -> list[str]:
             out.append("von_mises concentration update did not converge")
     if fam == "student_t" and st & _native.MS_WARN_CEILING:
         out.append("student_t degrees of freedom clamped; near-Gaussian state")
+    if fam == "beta" and st & _native.MS_WARN_ITERCAP:
+        out.append("beta fit hit the iteration cap before tolerance")
+    if fam == "weibull" and st & _native.MS_WARN_NEWTON:
+        out.append("weibull shape update did not converge; using moment seed")
+    if fam == "chi_squared" and st & _native.MS_WARN_NEWTON:
+        out.append("chi_squared update did not converge; using mean seed")
+    if fam == "negative_binomial":
+        if st & _native.MS_WARN_BOUNDARY:
+            out.append("negative_binomial data is underdispersed; returning near-Poisson boundary fit")
+        if st & _native.MS_WARN_CEILING:
+            out.append("negative_binomial dispersion clamped; data is near-Poisson")
+        if st & _native.MS_WARN_NEWTON:
+            out.append("negative_binomial dispersion update did not converge")
     return out
 
 
-def apply_mstep_status(st: np.ndarray, fams, stacklevel: int = 2) -> list[int]:
+def _natural(em) -> np.ndarray:
+    """Natural parameters of a device record (categorical keeps log p_k in
+    its 8 slots: p = exp(log p)))."""
+    if int(em["family"]) == _native.FAM["categorical"]:
+        m = int(em["reserved"])
+        return np.exp(np.concatenate([em["p"], em["c"]]))[:m]
+    return em["p"]
+
+
+def apply_mstep_status(st: np.ndarray, fams, stacklevel: int = 2, cats=None) -> list[int]:
     """Raise / warn for the per-state M-step status words the way
     m_step_emissions and the family fits do (training.py:130-148,
     distributions.py FitWarning sites); returns the collapsed states.
@@ -140,6 +180,9 @@ def apply_mstep_status(st: np.ndarray, fams, stacklevel: int = 2) -> list[int]:
             code = int(st[s * K + j])
             fam = _FAM_NAME[fams[s][j]]
             base = code & 0xFF
+            if base == _native.MS_ERR_CAT_CODE:
+                m = int(cats[s][j]) if cats is not None else 0
+                raise TrainingError(f"state {j}: categorical fit saw code >= {m}")
             if base >= 16:
                 raise TrainingError(f"state {j}: {_ERR_TEXT[base](fam)}")
             for msg in _warn_texts(fam, code):
@@ -160,7 +203,8 @@ def model_from_record(rec: np.ndarray, keep=None) -> HmmModel:
         if keep is not None and keep[j] is not None:
             ems.append(keep[j])
             continue
-        parts = [from_record(int(rec["em"][s, j]["family"]), rec["em"][s, j]["p"]) for s in range(ns)]
+        parts = [from_record(int(rec["em"][s, j]["family"]), _natural(rec["em"][s, j]),
+                             int(rec["em"][s, j]["reserved"])) for s in range(ns)]
         ems.append(parts[0] if ns == 1 else Joint(parts[0], parts[1]))
     pi = np.array(rec["pi"][:K], dtype=float)
     A = np.array(rec["A"][: K * K], dtype=float).reshape(K, K)
@@ -198,9 +242,12 @@ def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtyp
     student_streams = sorted({s for s, _ in student})
     var_fams = (_native.FAM["gaussian"], _native.FAM["gamma"], _native.FAM["student_t"])
     var_streams = [s for s in range(ns) if any(f in var_fams for f in fams[s])]
+    ext_streams = [s for s in range(ns) if any(f >= _native.FAM["lognormal"] for f in fams[s])]
+    cats = [[int(dm_cur.host["em"][s, j]["reserved"]) for j in range(K)] for s in range(ns)]
     dev = batch.y0.device
     # gamma is materialised for the exact second passes (variance, ECME guard)
-    need_gamma = bool(student) or bool(var_streams)
+    # and the weighted-sample fits of the families 6..15
+    need_gamma = bool(student) or bool(var_streams) or bool(ext_streams)
     out = engine.forward_backward(batch, dm_cur, alpha=False, beta=False, gamma=need_gamma,
                                   stats=True)
     totals = torch.empty(out.partials.shape[1] + 1, dtype=torch.float64, device=dev)
@@ -241,7 +288,9 @@ def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtyp
                 if int(need_more.item()) == 0:
                     break
                 ncand = _native.GUARD_CANDIDATES
-        collapsed = apply_mstep_status(status.cpu().numpy(), fams, stacklevel=3)
+        for s in ext_streams:
+            engine.ext_fit(batch, dm_next, out.gamma, s, guard, status, need_more)
+        collapsed = apply_mstep_status(status.cpu().numpy(), fams, stacklevel=3, cats=cats)
         collapsed_states.extend((iteration, j) for j in collapsed)
         # a collapsed state keeps its distribution object (m_step_emissions
         # returns ``dist`` itself, training.py:139-141)
