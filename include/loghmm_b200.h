@@ -295,6 +295,17 @@ int32_t loghmm_student_guard_select(loghmm_model_t* model_out, int32_t K, int32_
                                     int32_t n_candidates, double* guard_state, const double* sums,
                                     int32_t* status, int32_t* need_more, void* stream);
 
+/* default_initial_model (training.py:239-282) on the device: for the pooled
+ * observations SORTED ascending (fp64, N values) and the np.array_split into
+ * K bins, one row of LOGHMM_BIN_SLOTS doubles per bin (two-pass moments about
+ * the bin mean, as distributions.py _weighted_mean_var):
+ *   [0] n  [1] mean  [2] var  [3] mean log y (y>0)  [4] var log y  [5] sum sin y
+ *   [6] sum cos y  [7] sum y^2  [8] min  [9] max  [10] #(y<=0)  [11] #(y<0)
+ *   [12] #(y outside (0,1))  [13] #(y<0 or non-integral)  [14..21] #(y == c), c < 8 */
+#define LOGHMM_BIN_SLOTS 22
+int32_t loghmm_bin_moments(const double* pooled_sorted, int64_t N, int32_t K, double* out,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

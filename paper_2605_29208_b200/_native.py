@@ -74,6 +74,7 @@ MS_WARN_ITERCAP = 1 << 11
 MS_STUDENT_GUARD = 1 << 12
 MS_EXT_FIT = 1 << 13
 EXT_MAX_PASSES = 64
+BIN_SLOTS = 22
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -110,6 +111,7 @@ _SIGNATURES = {
         _i32,
         [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp],
     ),
+    "loghmm_bin_moments": (_i32, [_vp, _i64, _i32, _vp, _vp]),
     "loghmm_ext_fit_pass": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "loghmm_variance_partial": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
     "loghmm_variance_finish": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp, _vp]),

@@ -17,8 +17,9 @@ path on the B200 core, and hands back the reference's own result types:
 Rebound entry points (the functions SURVEY.md §8(b) lists for the path):
 ``inference.emission_log_matrix`` (:122), ``forward_log`` (:148),
 ``backward_log`` (:154), ``posteriors`` (:161), ``viterbi`` (:191),
-``training.baum_welch`` (:160) and ``training.score_model`` (:89), plus the
-package-level re-exports.  Exceptions and warnings are re-raised as the
+``training.baum_welch`` (:160), ``training.score_model`` (:89),
+``training.default_initial_model`` (:239) and ``model_io.read_sequences``
+(:150), wherever the package bound them (package re-exports, cli.py).  Exceptions and warnings are re-raised as the
 reference's own classes (``InfeasibleSequenceError``, ``TrainingError``,
 ``FitWarning``) with the same messages.  A family the device does not
 evaluate raises NotImplementedError -- the shim never falls back to the CPU.
@@ -27,12 +28,14 @@ evaluate raises NotImplementedError -- the shim never falls back to the CPU.
 from __future__ import annotations
 
 import functools
+import sys
 import warnings
 
 import numpy as np
 
 from . import distributions as D
 from . import inference as I
+from . import seqio
 from . import training as Tr
 
 __all__ = ["to_device_model", "to_device_distribution", "install", "Installed"]
@@ -165,13 +168,36 @@ def install(pkg, dtype: str = "float64") -> Installed:
         s = Tr.score_model(to_device_model(model), [inf.validate_sequence(x) for x in data], dtype)
         return RefScore(s.log_likelihood, s.num_params, s.num_obs, s.aic, s.bic, s.aicc)
 
-    new = {"emission_log_matrix": emission_log_matrix, "forward_log": forward_log,
-           "backward_log": backward_log, "posteriors": posteriors, "viterbi": viterbi}
-    new_t = {"baum_welch": baum_welch, "score_model": score_model}
-    saved = {}
-    for mod, table in ((inf, new), (trn, new_t), (pkg, {**new, **new_t})):
-        for name, fn in table.items():
+    @translate
+    def default_initial_model(num_states, families, data):
+        fams = [families] if isinstance(families, str) else list(families)
+        dev = Tr.default_initial_model(num_states, families, data)
+        ems = []
+        for j, d in enumerate(dev.emissions):
+            ref_cls = dst.FAMILIES[fams[j] if len(fams) > 1 else fams[0]]
+            ems.append(_to_reference_distribution(ref_cls, d))
+        return inf.HmmModel(dev.initial, dev.transitions, tuple(ems))
+
+    def read_sequences(source, column=0, delimiter=","):
+        return seqio.read_sequences(source, column=column, delimiter=delimiter)
+
+    table = {"emission_log_matrix": emission_log_matrix, "forward_log": forward_log,
+             "backward_log": backward_log, "posteriors": posteriors, "viterbi": viterbi,
+             "baum_welch": baum_welch, "score_model": score_model,
+             "default_initial_model": default_initial_model, "read_sequences": read_sequences}
+    # every module of the package that bound one of these names (the CLI
+    # imports them by name, cli.py:19-28) gets the drop-in
+    originals = {}
+    for mod in (inf, trn, pkg.model_io):
+        for name in table:
             if hasattr(mod, name):
-                saved[(mod, name)] = getattr(mod, name)
+                originals.setdefault(name, getattr(mod, name))
+    saved = {}
+    mods = [m for n, m in list(sys.modules.items()) if m is not None and (n == pkg.__name__ or n.startswith(pkg.__name__ + "."))]
+    for mod in mods:
+        for name, fn in table.items():
+            cur = getattr(mod, name, None)
+            if cur is not None and cur is originals.get(name):
+                saved[(mod, name)] = cur
                 setattr(mod, name, fn)
     return Installed(pkg, saved)

@@ -328,38 +328,93 @@ def score_model(model: HmmModel, data, dtype="float64") -> ModelScore:
 
 
 # ---------------------------------------------------------------------------
-# host-side initialisation (training.py:239-282; distributions.py:1114-1176)
+# default_initial_model on the device (training.py:239-282)
 # ---------------------------------------------------------------------------
-def _mean_var(y: np.ndarray):
-    n = float(y.size)
-    w = np.ones_like(y)
-    mean = float(np.dot(w, y) / n)
-    var = float(np.dot(w, (y - mean) ** 2) / n)
-    return n, mean, var
+_SUPPORT_SEED = {  # distributions.py:623-629 texts raised by moment_seed
+    "positive": "{} fit requires strictly positive observations",
+    "unit": "{} fit requires observations strictly inside (0, 1)",
+    "integer": "{} fit requires non-negative integer observations",
+}
 
 
-def _moment_seed(family: str, y: np.ndarray) -> Distribution:
-    n, mean, var = _mean_var(y)
+def _seed_from_moments(family: str, row: np.ndarray, pool: np.ndarray, num_categories) -> Distribution:
+    """moment_seed (distributions.py:1130-1176) from one bin's device
+    moments (loghmm_bin_moments row; ``pool`` = the row of the whole pool,
+    used by uniform / pareto, whose M-steps pin the global range)."""
+    from .distributions import (
+        NEGBINOM_R_CEILING, Beta, Categorical, ChiSquared, Exponential, LogNormal, NegativeBinomial,
+        Pareto, Rayleigh, Uniform, Weibull)
+
+    n, mean, var = float(row[0]), float(row[1]), float(row[2])
     sd = max(math.sqrt(var), SCALE_FLOOR)
+
+    def need(kind, bad):
+        if bad > 0:
+            raise ValueError(_SUPPORT_SEED[kind].format(family))
+
     if family == "gaussian":
         return Gaussian(mean, sd)
+    if family == "lognormal":
+        need("positive", row[10])
+        return LogNormal(float(row[3]), max(math.sqrt(float(row[4])), SCALE_FLOOR))
+    if family == "exponential":
+        return Exponential(1.0 / max(mean, SCALE_FLOOR))
     if family == "poisson":
         return Poisson(max(mean, SCALE_FLOOR))
+    if family == "rayleigh":
+        return Rayleigh(max(math.sqrt(float(row[7]) / (2.0 * n)), SCALE_FLOOR))
+    if family == "uniform":  # fit_uniform on the pool (distributions.py:676-684)
+        lo, hi = float(pool[8]), float(pool[9])
+        if hi <= lo:
+            hi = lo + SCALE_FLOOR
+        return Uniform(lo, hi)
+    if family == "categorical":  # fit_categorical (distributions.py:687-699)
+        need("integer", row[13])
+        if num_categories > 8:
+            raise ValueError(f"categorical with {num_categories} categories: the device record holds at most 8")
+        counts = np.asarray(row[14:14 + num_categories], dtype=float)
+        probs = counts / n
+        probs = probs / probs.sum()
+        return Categorical(tuple(float(p) for p in probs))
     if family == "von_mises":
-        w = np.ones_like(y)
-        s = float(np.dot(w, np.sin(y)))
-        c = float(np.dot(w, np.cos(y)))
-        mu = math.atan2(s, c)
+        s_, c_ = float(row[5]), float(row[6])
+        mu = math.atan2(s_, c_)
         if mu <= -math.pi:
             mu = math.pi
-        rbar = min(math.hypot(s, c) / n, 1.0 - 1e-9)
+        rbar = min(math.hypot(s_, c_) / n, 1.0 - 1e-9)
         kappa = rbar * (2.0 - rbar * rbar) / (1.0 - rbar * rbar)
         return VonMises(mu, min(kappa, VONMISES_KAPPA_CEILING))
     if family == "gamma":
-        if (y <= 0).any():
-            raise ValueError("gamma fit requires strictly positive observations")
+        need("positive", row[10])
         shape = mean * mean / var if var > 0 else 1.0
         return Gamma(max(shape, SCALE_FLOOR), max(shape, SCALE_FLOOR) / max(mean, SCALE_FLOOR))
+    if family == "beta":
+        need("unit", row[12])
+        scale = mean * (1.0 - mean) / var - 1.0 if var > 0 else -1.0
+        if scale <= 0:
+            return Beta(1.0, 1.0)
+        return Beta(mean * scale, (1.0 - mean) * scale)
+    if family == "weibull":
+        need("positive", row[10])
+        k = (mean / sd) ** 1.086 if var > 0 else 1.0
+        scale = mean / math.exp(math.lgamma(1.0 + 1.0 / k))
+        return Weibull(k, max(scale, SCALE_FLOOR))
+    if family == "negative_binomial":
+        need("integer", row[13])
+        if mean <= 0:
+            raise ValueError("negative_binomial seed is degenerate: zero mean")
+        r = mean * mean / (var - mean) if var > mean else NEGBINOM_R_CEILING
+        return NegativeBinomial(r, r / (r + mean))
+    if family == "chi_squared":
+        need("positive", row[10])
+        return ChiSquared(max(mean, SCALE_FLOOR))
+    if family == "pareto":  # fit_pareto on the pool (distributions.py:702-710)
+        need("positive", pool[10])
+        npool, xm = float(pool[0]), float(pool[8])
+        denom = npool * (float(pool[3]) - math.log(xm))
+        if denom <= 0.0:
+            raise ValueError("pareto fit is degenerate: all weighted observations equal the minimum")
+        return Pareto(xm, npool / denom)
     if family == "student_t":
         return StudentT(mean, sd, 10.0)
     raise ValueError(f"unknown family '{family}'")
@@ -368,7 +423,9 @@ def _moment_seed(family: str, y: np.ndarray) -> Distribution:
 def default_initial_model(num_states: int, families, data) -> HmmModel:
     """Deterministic starting model: pooled observations sorted and split into
     quantile bins, one per state, each seeded from its bin's moments; uniform
-    start with sticky diagonals (training.py:239-282)."""
+    start with sticky diagonals (training.py:239-282).  The pool is sorted on
+    the device and loghmm_bin_moments reduces every bin in one launch; only
+    K rows of moments come back to the host."""
     if num_states < 1:
         raise ValueError("num_states must be positive")
     if isinstance(families, str):
@@ -378,18 +435,25 @@ def default_initial_model(num_states: int, families, data) -> HmmModel:
         families = families * num_states
     if len(families) != num_states:
         raise ValueError(f"expected 1 or {num_states} family names, got {len(families)}")
-    if isinstance(data, np.ndarray) and data.ndim == 1:
-        data = [data]
-    seqs = [np.asarray(s, dtype=float) for s in data]
-    if not seqs:
+    if isinstance(data, (list, tuple)) and len(data) == 0:
         raise TrainingError("training data contains no sequences")
-    pooled = np.sort(np.concatenate([s.reshape(-1) for s in seqs]))
-    bins = np.array_split(pooled, num_states)
-    emissions = []
-    for family, chunk in zip(families, bins):
-        if chunk.size == 0:
-            raise TrainingError("more states than observations; cannot seed bins")
-        emissions.append(_moment_seed(family, chunk))
+    batch = engine.make_batch(data, 1, "float64")
+    if bool(torch.isnan(batch.y0).any()):
+        raise ValueError("observation sequence contains NaN")
+    N = batch.N
+    if N < num_states:
+        raise TrainingError("more states than observations; cannot seed bins")
+    pooled = torch.sort(batch.y0).values  # device radix sort (np.sort of the pool)
+    L = _native.lib()
+    rows = torch.empty((num_states, _native.BIN_SLOTS), dtype=torch.float64, device=pooled.device)
+    _native.check(L.loghmm_bin_moments(pooled.data_ptr(), N, num_states, rows.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream), "loghmm_bin_moments")
+    pool = torch.empty((1, _native.BIN_SLOTS), dtype=torch.float64, device=pooled.device)
+    _native.check(L.loghmm_bin_moments(pooled.data_ptr(), N, 1, pool.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream), "loghmm_bin_moments")
+    rows, pool = rows.cpu().numpy(), pool.cpu().numpy()[0]
+    num_categories = int(pool[9]) + 1 if "categorical" in families else None
+    emissions = [_seed_from_moments(f, rows[j], pool, num_categories) for j, f in enumerate(families)]
     pi = np.full(num_states, 1.0 / num_states)
     if num_states == 1:
         a = np.array([[1.0]])

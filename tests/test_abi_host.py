@@ -12,7 +12,7 @@ from paper_2605_29208_b200 import _native
 from paper_2605_29208_b200.distributions import Gamma, Gaussian, Joint, Poisson, StudentT, VonMises
 from paper_2605_29208_b200.engine import encode_model
 from paper_2605_29208_b200.inference import HmmModel
-from paper_2605_29208_b200.training import TrainingConfig, default_initial_model
+from paper_2605_29208_b200.training import TrainingConfig
 
 ROOT = Path(__file__).resolve().parents[1]
 
@@ -73,15 +73,6 @@ def test_encode_joint_model():
     assert rec["em"][0, 0]["family"] == _native.FAM["gamma"]
     assert rec["em"][1, 0]["family"] == _native.FAM["von_mises"]
     assert rec["em"][0, 0]["c"][1] == 1.0
-
-
-def test_default_initial_model_matches_reference_rule():
-    y = np.array([3.0, 1.0, 2.0, 10.0, 12.0, 11.0, 0.0])
-    m = default_initial_model(2, "poisson", [y])
-    rates = [d.rate for d in m.emissions]
-    bins = np.array_split(np.sort(y), 2)
-    assert rates == [float(np.mean(b)) for b in bins]
-    assert np.allclose(m.transitions, [[0.9, 0.1], [0.1, 0.9]])
 
 
 def test_no_cpu_fallback_without_gpu():
