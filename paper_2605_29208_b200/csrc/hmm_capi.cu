@@ -135,29 +135,28 @@ static cudaError_t dispatch_fb_small(int K, const FBArgs& a, int cfg, bool gl, d
   }
 }
 
-// Two-lane Viterbi (K in [2,4], LOGHMM_VIT_ALGO=pair) geometry: nibble
-// backpointer words in smem.  Kept as an alternative decomposition; the K-lane
-// kernel is faster on B200 (twice the warps, shorter per-step issue).
-static bool vit2_ok(int K, int64_t max_T, int* wpb, size_t* smem, int* warp_words) {
+// Chain-warp Viterbi (hmm_viterbi3.cuh; K in [2,4], sequences whose
+// backpointer bytes fit in shared memory).  LOGHMM_VIT_ALGO=lanes forces the
+// K-lanes-per-sequence kernel; LOGHMM_VIT_NW picks 8 or 16 warps per CTA.
+static bool vit3_ok(int K, int esz, int64_t max_T, int* nw, size_t* smem) {
   if (K < 2 || K > 4) return false;
   const char* env = getenv("LOGHMM_VIT_ALGO");
-  if (!env || strcmp(env, "pair") != 0) return false;  // K-lane kernel is the default
-  const int64_t words = kVit2StageWords + ((max_T + 7) / 8) * kWarp;
-  const int64_t bytes = ((words + 3) & ~3LL) * 4;
-  if (bytes > 100 * 1024) return false;
-  *warp_words = (int)((words + 3) & ~3LL);
-  *wpb = (int)std::max<int64_t>(1, std::min<int64_t>(4, (200 * 1024) / bytes));
-  *smem = (size_t)bytes * (*wpb);
+  if (env && strcmp(env, "lanes") == 0) return false;
+  const size_t bytes = v3_smem_bytes(esz, max_T);
+  if (bytes > 200 * 1024) return false;
+  *smem = bytes;
+  *nw = 8;
+  if (const char* e2 = getenv("LOGHMM_VIT_NW")) *nw = atoi(e2) >= 16 ? 16 : 8;
   return true;
 }
 
 template <typename R>
-static cudaError_t dispatch_vit2(int K, const VitArgs& a, int cfg, dim3 grid, dim3 block,
-                                 size_t smem, cudaStream_t st) {
+static cudaError_t dispatch_vit3(int K, const VitArgs& a, int cfg, int nw, dim3 grid, size_t smem,
+                                 cudaStream_t st) {
   switch (K) {
-    case 2: return launch_vit2<R, 2>(a, cfg, grid, block, smem, st);
-    case 3: return launch_vit2<R, 3>(a, cfg, grid, block, smem, st);
-    default: return launch_vit2<R, 4>(a, cfg, grid, block, smem, st);
+    case 2: return launch_vit3<R, 2>(a, cfg, nw, grid, smem, st);
+    case 3: return launch_vit3<R, 3>(a, cfg, nw, grid, smem, st);
+    default: return launch_vit3<R, 4>(a, cfg, nw, grid, smem, st);
   }
 }
 
@@ -489,16 +488,14 @@ int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm
   a.back = back;
   a.flags = flags;
   cudaError_t e;
-  int v2_wpb = 0, v2_words = 0;
-  size_t v2_smem = 0;
-  if (vit2_ok(K, max_T, &v2_wpb, &v2_smem, &v2_words)) {
-    a.warp_smem_words = v2_words;
+  int v3_nw = 0;
+  size_t v3_smem = 0;
+  if (vit3_ok(K, dtype == LOGHMM_F64 ? 8 : 4, max_T, &v3_nw, &v3_smem)) {
     int fams = 0;
     const int cfg = cfg_of(h_desc, &fams);
-    const int64_t warps = (B + 15) / 16;
-    dim3 grid((unsigned)((warps + v2_wpb - 1) / v2_wpb)), block(32 * v2_wpb);
-    e = dtype == LOGHMM_F64 ? dispatch_vit2<double>(K, a, cfg, grid, block, v2_smem, st)
-                            : dispatch_vit2<float>(K, a, cfg, grid, block, v2_smem, st);
+    dim3 grid((unsigned)((B + kV3Seq - 1) / kV3Seq));
+    e = dtype == LOGHMM_F64 ? dispatch_vit3<double>(K, a, cfg, v3_nw, grid, v3_smem, st)
+                            : dispatch_vit3<float>(K, a, cfg, v3_nw, grid, v3_smem, st);
   } else if (K <= 8) {
     int fams = 0;
     const int cfg = cfg_of(h_desc, &fams);

@@ -278,6 +278,21 @@ struct V {
   }
 };
 
+// Per-CTA shared model table, computed once by the first K threads of the
+// CTA (column j each): column-scaled A, log2 column scales, log2 pi, and the
+// Gaussian emission constants of the log2 form (Em2).
+template <int K>
+struct FBCTab {
+  static constexpr int AM = 0;            // [K][K] column-scaled A
+  static constexpr int LC = K * K;        // [K] log2 c_j
+  static constexpr int LPI = LC + K;      // [K] log2 pi_j
+  static constexpr int GA = LPI + K;      // [K] s_j = sqrt(log2(e)/2)/sigma_j
+  static constexpr int GO = GA + K;       // [K] -mu_j s_j
+  static constexpr int GR = GO + K;       // [K] c_j log2(e)
+  static constexpr int MU = GR + K;       // [K] mu_j
+  static constexpr int N = MU + K;
+};
+
 // Emission log2-densities of all states (u_j = log2 b_j(y)).  The Gaussian is
 // rewritten as u = c - w^2 with w = y*s - mu*s, s = sqrt(log2(e)/2)/sigma.
 // eval() returns v_j = u_j + lc_j, the log2-density plus the log2 column
@@ -288,21 +303,27 @@ struct V {
 template <typename R, int K, int CFG>
 struct Em2 {
   Emit<R, K, CFG> em;
-  R ga[K], go[K], gc[K], lc[K];
+  R ga[K], go[K], gc[K], gr[K], lc[K], mu[K];
+  // tab: the CTA's shared model table (FBCTab layout); the Gaussian
+  // configuration reads its per-state constants from it (computed once per
+  // CTA), the others load the family parameters themselves
   __device__ __forceinline__ void load(const loghmm_model_t* m, int n_streams, int fams,
-                                       const double* lut, int lut_n, const R (&lc2)[K]) {
-    em.load(m, n_streams, fams, lut, lut_n);
+                                       const double* lut, int lut_n, const R (&lc2)[K], const R* tab) {
 #pragma unroll
     for (int j = 0; j < K; ++j) lc[j] = lc2[j];
     if constexpr (CFG == kCfgGauss) {
-      const double h = sqrt(0.5 * 1.4426950408889634);
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        const double s = h / m->em[0][j].p[1];
-        ga[j] = (R)s;
-        go[j] = (R)(-m->em[0][j].p[0] * s);
-        gc[j] = (R)(m->em[0][j].c[0] * 1.4426950408889634) + lc2[j];
+        ga[j] = tab[FBCTab<K>::GA + j];
+        go[j] = tab[FBCTab<K>::GO + j];
+        gr[j] = tab[FBCTab<K>::GR + j];
+        gc[j] = gr[j] + lc2[j];
+        mu[j] = tab[FBCTab<K>::MU + j];
       }
+    } else {
+      em.load(m, n_streams, fams, lut, lut_n);
+#pragma unroll
+      for (int j = 0; j < K; ++j) mu[j] = em.e0[j].q[0];
     }
   }
   __device__ __forceinline__ void eval(R y0, R y1, ObsFeat<R>& f0, ObsFeat<R>& f1, R (&u)[K],
@@ -321,11 +342,18 @@ struct Em2 {
     }
   }
   __device__ __forceinline__ void eval_raw(R y0, R y1, R (&u)[K], bool& oob) const {
-    ObsFeat<R> f0, f1;
-    R lb[K];
-    em.eval(y0, y1, f0, f1, lb, oob);
+    if constexpr (CFG == kCfgGauss) {
+      R w[K], w2[K];
+      V<R, K>::fma_s(w, y0, ga, go);
+      V<R, K>::mul(w2, w, w);
+      V<R, K>::sub(u, gr, w2);
+    } else {
+      ObsFeat<R> f0, f1;
+      R lb[K];
+      em.eval(y0, y1, f0, f1, lb, oob);
 #pragma unroll
-    for (int j = 0; j < K; ++j) u[j] = lb[j] * R(1.4426950408889634);
+      for (int j = 0; j < K; ++j) u[j] = lb[j] * R(1.4426950408889634);
+    }
   }
 };
 
@@ -437,11 +465,40 @@ __global__ void __launch_bounds__(128)
   constexpr R kFloor = sizeof(R) == 4 ? R(-1e30) : R(-1e300);  // finite stand-in for max of all -inf
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_tmem;
+  __shared__ R s_tab[FBCTab<K>::N];
 
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   const bool valid = b < a.B;
+
+  // model table: thread j < K fills column j (one global round trip and one
+  // set of double-precision constants per CTA instead of per thread)
+  if (threadIdx.x < K) {
+    const loghmm_model_t* __restrict__ mt = a.model;
+    const int j = threadIdx.x;
+    R col[K], c = R(0);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      col[i] = (R)mt->A[i * K + j];
+      c = c > col[i] ? c : col[i];
+    }
+    const bool nz = c > R(0);
+    const R rc = nz ? N::frcp(c) : R(0);
+#pragma unroll
+    for (int i = 0; i < K; ++i) s_tab[FBCTab<K>::AM + i * K + j] = col[i] * rc;
+    if constexpr (sizeof(R) == 4) s_tab[FBCTab<K>::LC + j] = nz ? N::flg2(c) : N::ninf();
+    else s_tab[FBCTab<K>::LC + j] = nz ? (R)log2((double)c) : N::ninf();
+    s_tab[FBCTab<K>::LPI + j] = (R)(mt->log_pi[j] * 1.4426950408889634);
+    if constexpr (CFG == kCfgGauss) {
+      const double h = sqrt(0.5 * 1.4426950408889634);
+      const double sg = h / mt->em[0][j].p[1];
+      s_tab[FBCTab<K>::GA + j] = (R)sg;
+      s_tab[FBCTab<K>::GO + j] = (R)(-mt->em[0][j].p[0] * sg);
+      s_tab[FBCTab<K>::GR + j] = (R)(mt->em[0][j].c[0] * 1.4426950408889634);
+      s_tab[FBCTab<K>::MU + j] = (R)mt->em[0][j].p[0];
+    }
+  }
 
   uint32_t tbase = 0;
   if constexpr (TM) {
@@ -456,6 +513,8 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
     tm_fence_after();
     tbase = s_tmem + ((uint32_t)(32 * wib) << 16);
+  } else {
+    __syncthreads();  // model table
   }
 
   if (valid) {
@@ -493,8 +552,11 @@ __global__ void __launch_bounds__(128)
 
     // ---- model -----------------------------------------------------------
     const loghmm_model_t* __restrict__ md = a.model;
-    R Am[K][K], lc2[K];  // column-scaled A (load_colscaled), log2 c_j
-    load_colscaled<R, K>(md, Am, lc2, 1.0);
+    R Am[K][K], lc2[K];  // column-scaled A, log2 c_j (from the CTA's table)
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) Am[i][j] = s_tab[FBCTab<K>::AM + i * K + j];
     R minA = R(1);
 #pragma unroll
     for (int i = 0; i < K; ++i)
@@ -502,18 +564,21 @@ __global__ void __launch_bounds__(128)
       for (int j = 0; j < K; ++j) minA = fmin(Am[i][j], minA);
     R lpi2[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) lpi2[j] = (R)(md->log_pi[j] * 1.4426950408889634);
+    for (int j = 0; j < K; ++j) {
+      lc2[j] = s_tab[FBCTab<K>::LC + j];
+      lpi2[j] = s_tab[FBCTab<K>::LPI + j];
+    }
     Em2<R, K, CFG> em;
-    em.load(md, a.n_streams, a.stream_fams, a.lut, a.lut_n, lc2);
+    em.load(md, a.n_streams, a.stream_fams, a.lut, a.lut_n, lc2, s_tab);
     // Pass-1 operator renormalisation every nn steps: its max entry shrinks
     // by at most min(A) per step, so nn steps stay above 2^-100 (fp32) /
     // 2^-900 (fp64).  (Pass 2 renormalises every step through the emission
     // shift instead.)
     int nn = 1;
     if (minA > R(0)) {
-      const double lg = -log2((double)minA);
-      const double budget = sizeof(R) == 4 ? 100.0 : 900.0;
-      nn = lg <= 0.0 ? 8 : (int)fmin(8.0, fmax(1.0, floor(budget / lg)));
+      const float lg = -Num<float>::flg2((float)minA);
+      const float budget = sizeof(R) == 4 ? 100.0f : 900.0f;
+      nn = lg <= 0.0f ? 8 : (int)fminf(8.0f, fmaxf(1.0f, floorf(budget / lg)));
     }
     // pass-1 operator: every step (nn < 4) or every 1 / 2 four-step groups
     const bool rn_step = nn < 4;
@@ -786,7 +851,7 @@ __global__ void __launch_bounds__(128)
     for (int i = 0; i < K; ++i) {
       pg[i] = R(0);
       gs0[i] = gs1[i] = gs2[i] = R(0);
-      mu[i] = em.em.e0[i].q[0];
+      mu[i] = em.mu[i];
 #pragma unroll
       for (int j = 0; j < K; ++j) X[i][j] = R(0);
 #pragma unroll
@@ -1046,32 +1111,26 @@ __global__ void __launch_bounds__(128)
       }
     }
     if (a.partials) {
+      // Per-sequence statistics row: every lane holds its chunk's share of Q
+      // quantities; they are summed over the 32 lanes 32 quantities at a time
+      // through a [32][33] shared tile (lane q adds column q in lane order —
+      // fixed order, bit-reproducible) and written as coalesced doubles.
       double* row = a.partials + b * a.stats_width;
-      int idx = 0;
-#pragma unroll
-      for (int i = 0; i < K; ++i)
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const R v = warp_sum(X[i][j]);
-          if (lane == (idx & 31)) row[idx] = (double)v * (double)Am[i][j];
-          ++idx;
-        }
-      // gamma totals over t < T-1 = all-step mass minus the last posterior
-#pragma unroll
+      constexpr int NSL = TR::S * K * LOGHMM_NSLOT;
+      constexpr int Q = K * K + 2 * K + NSL;
       R glast[K], g0[K];
       SVec<R, K>::ld(myGl, glast);
       SVec<R, K>::ld(myG0, g0);
+      R vals[Q];
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = 0; j < K; ++j) vals[i * K + j] = X[i][j];
+      // gamma totals over t < T-1 = all-step mass minus the last posterior
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        const R v = warp_sum(st[0][j][0] - (lane == C - 1 ? glast[j] : R(0)));
-        if (lane == (idx & 31)) row[idx] = (double)v;
-        ++idx;
-      }
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const R v = __shfl_sync(kFull, g0[j], 0);
-        if (lane == (idx & 31)) row[idx] = (double)v;
-        ++idx;
+        vals[K * K + j] = st[0][j][0] - (lane == C - 1 ? glast[j] : R(0));
+        vals[K * K + K + j] = lane == 0 ? g0[j] : R(0);
       }
 #pragma unroll
       for (int s = 0; s < TR::S; ++s)
@@ -1080,13 +1139,29 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
           for (int q = 0; q < LOGHMM_NSLOT; ++q) {
             const int ns = s == 0 ? TR::NS0 : TR::NS1;
-            R v = R(0);
-            if (q < ns) v = warp_sum(st[s][j][q]);
-            if (lane == (idx & 31)) row[idx] = (double)v;
-            ++idx;
+            vals[K * K + 2 * K + (s * K + j) * LOGHMM_NSLOT + q] = q < ns ? st[s][j][q] : R(0);
           }
-      for (; idx < a.stats_width; ++idx)
-        if (lane == (idx & 31)) row[idx] = 0.0;
+      R* tile = wsm;  // the output stages are idle now (>= 32 * 33 elements)
+      __syncwarp();
+#pragma unroll
+      for (int r0 = 0; r0 < Q; r0 += 32) {
+        const int n = Q - r0 < 32 ? Q - r0 : 32;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (r0 + q < Q) tile[lane * 33 + q] = vals[r0 + q < Q ? r0 + q : 0];
+        __syncwarp();
+        if (lane < n) {
+          R acc = tile[lane];
+#pragma unroll 8
+          for (int l = 1; l < 32; ++l) acc += tile[l * 33 + lane];
+          const int idx = r0 + lane;
+          double v = (double)acc;
+          if (idx < K * K) v *= (double)s_tab[FBCTab<K>::AM + idx];
+          row[idx] = v;
+        }
+        __syncwarp();
+      }
+      for (int idx = Q + lane; idx < a.stats_width; idx += kWarp) row[idx] = 0.0;
     }
   }
 

@@ -9,7 +9,7 @@
 #include "hmm_fb.cuh"
 #define LHMM_HAS_FB 1
 #elif defined(LHMM_ONLY_VIT)
-#include "hmm_viterbi2.cuh"
+#include "hmm_viterbi3.cuh"
 #define LHMM_HAS_VIT 1
 #elif defined(LHMM_ONLY_FBC)
 #include "hmm_fbc.cuh"
@@ -18,7 +18,7 @@
 #include "hmm_fb.cuh"
 #include "hmm_fbc.cuh"
 #include "hmm_viterbi.cuh"
-#include "hmm_viterbi2.cuh"
+#include "hmm_viterbi3.cuh"
 #define LHMM_HAS_FB 1
 #define LHMM_HAS_VIT 1
 #define LHMM_HAS_FBC 1
@@ -91,31 +91,36 @@ cudaError_t launch_vit_small(const VitArgs& a, int cfg, bool global, dim3 grid, 
                 : launch_vit_cfg<R, K, false>(a, cfg, grid, block, smem, st);
 }
 
-template <typename R, int K, int CFG>
-static cudaError_t launch_vit2_one(const VitArgs& a, dim3 grid, dim3 block, size_t smem,
-                                   cudaStream_t st) {
+template <typename R, int K, int CFG, int NW>
+static cudaError_t launch_vit3_one(const VitArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   if constexpr (K >= 2 && K <= 4) {
-    auto fn = viterbi2_kernel<R, K, CFG>;
+    auto fn = viterbi_chain_kernel<R, K, CFG, NW>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    fn<<<grid, block, smem, st>>>(a);
+    fn<<<grid, dim3(32 * NW), smem, st>>>(a);
     return cudaGetLastError();
   } else {
     return cudaErrorInvalidValue;
   }
 }
 
+template <typename R, int K, int CFG>
+static cudaError_t launch_vit3_nw(const VitArgs& a, int nw, dim3 grid, size_t smem, cudaStream_t st) {
+  if (nw >= 16) return launch_vit3_one<R, K, CFG, 16>(a, grid, smem, st);
+  return launch_vit3_one<R, K, CFG, 8>(a, grid, smem, st);
+}
+
+// chain-warp Viterbi (hmm_viterbi3.cuh): nw warps per CTA (8 or 16)
 template <typename R, int K>
-cudaError_t launch_vit2(const VitArgs& a, int cfg, dim3 grid, dim3 block, size_t smem,
-                        cudaStream_t st) {
+cudaError_t launch_vit3(const VitArgs& a, int cfg, int nw, dim3 grid, size_t smem, cudaStream_t st) {
   switch (cfg) {
-    case kCfgGauss: return launch_vit2_one<R, K, kCfgGauss>(a, grid, block, smem, st);
-    case kCfgStudent: return launch_vit2_one<R, K, kCfgStudent>(a, grid, block, smem, st);
-    case kCfgGamma: return launch_vit2_one<R, K, kCfgGamma>(a, grid, block, smem, st);
-    case kCfgVonMises: return launch_vit2_one<R, K, kCfgVonMises>(a, grid, block, smem, st);
-    case kCfgPoisson: return launch_vit2_one<R, K, kCfgPoisson>(a, grid, block, smem, st);
-    case kCfgGammaVM: return launch_vit2_one<R, K, kCfgGammaVM>(a, grid, block, smem, st);
-    default: return launch_vit2_one<R, K, kCfgMixed>(a, grid, block, smem, st);
+    case kCfgGauss: return launch_vit3_nw<R, K, kCfgGauss>(a, nw, grid, smem, st);
+    case kCfgStudent: return launch_vit3_nw<R, K, kCfgStudent>(a, nw, grid, smem, st);
+    case kCfgGamma: return launch_vit3_nw<R, K, kCfgGamma>(a, nw, grid, smem, st);
+    case kCfgVonMises: return launch_vit3_nw<R, K, kCfgVonMises>(a, nw, grid, smem, st);
+    case kCfgPoisson: return launch_vit3_nw<R, K, kCfgPoisson>(a, nw, grid, smem, st);
+    case kCfgGammaVM: return launch_vit3_nw<R, K, kCfgGammaVM>(a, nw, grid, smem, st);
+    default: return launch_vit3_nw<R, K, kCfgMixed>(a, nw, grid, smem, st);
   }
 }
 #endif  // LHMM_HAS_VIT
@@ -160,7 +165,7 @@ int fb_chunk_warp_elems(int L) { return FBCGeom<R, K>::warp_elems(L); }
 #define LHMM_INST_VIT(R, K)                                                                  \
   template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
                                               cudaStream_t);                                 \
-  template cudaError_t launch_vit2<R, K>(const VitArgs&, int, dim3, dim3, size_t, cudaStream_t);
+  template cudaError_t launch_vit3<R, K>(const VitArgs&, int, int, dim3, size_t, cudaStream_t);
 #define LHMM_INST_FBC(R, K)                                                                  \
   template cudaError_t launch_fb_chunk<R, K>(const FBCArgs&, int, dim3, dim3, size_t, cudaStream_t); \
   template int fb_chunk_warp_elems<R, K>(int);
@@ -170,7 +175,7 @@ int fb_chunk_warp_elems(int L) { return FBCGeom<R, K>::warp_elems(L); }
                                                     cudaStream_t);                                  \
   extern template cudaError_t launch_vit_small<R, K>(const VitArgs&, int, bool, dim3, dim3, size_t, \
                                                      cudaStream_t);                                 \
-  extern template cudaError_t launch_vit2<R, K>(const VitArgs&, int, dim3, dim3, size_t, cudaStream_t); \
+  extern template cudaError_t launch_vit3<R, K>(const VitArgs&, int, int, dim3, size_t, cudaStream_t); \
   extern template cudaError_t launch_fb_chunk<R, K>(const FBCArgs&, int, dim3, dim3, size_t, cudaStream_t); \
   extern template int fb_chunk_warp_elems<R, K>(int);
 
