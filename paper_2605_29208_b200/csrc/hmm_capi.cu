@@ -256,6 +256,8 @@ static cudaError_t launch_split(const FBArgs& a, int K, int KM, int lps, int64_t
   sw.qws = (char*)workspace + 2 * nk;
   sw.wws = (char*)workspace + 3 * nk;
   sw.seg_part = (double*)((char*)workspace + 4 * nk);
+  sw.sparse_ok = 1;
+  if (const char* env = getenv("LOGHMM_FBL_SPARSE")) sw.sparse_ok = atoi(env) != 0;
   const size_t ssm = (size_t)(2 * KM + 128 + kRing * 4 * KM) * sizeof(R);
   const R* lb = (const R*)lbw;
 #define LHMM_FBS(KMV)                                                                            \
@@ -304,8 +306,8 @@ size_t loghmm_fb_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N,
 
 size_t loghmm_viterbi_workspace_bytes(int32_t dtype, int32_t K, int64_t B, int64_t N,
                                       int64_t max_T) {
-  (void)dtype;
-  if (K > 8) return align256((size_t)N * K);
+  // large K: byte backpointer table + the precomputed emission log-densities
+  if (K > 8) return align256((size_t)N * K) + align256((size_t)N * K * (dtype == LOGHMM_F64 ? 8 : 4));
   VitGeom g = vit_geom(K, max_T);
   if (!g.global) return 0;
   const int64_t G = kWarp / K;
@@ -512,15 +514,20 @@ int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm
   } else {
     const int esz = dtype == LOGHMM_F64 ? 8 : 4;
     const int KM = K <= 16 ? 16 : K <= 32 ? 32 : 64;
+    // LOGHMM_VL_SPARSE=0 keeps banded models on the dense recursion (A/B, tests)
+    a.sparse_ok = 1;
+    if (const char* env = getenv("LOGHMM_VL_SPARSE")) a.sparse_ok = atoi(env) != 0;
     int vlps = 4;  // lanes per destination state (LOGHMM_VL_LPS: 1, 2 or 4)
     if (const char* env = getenv("LOGHMM_VL_LPS")) vlps = atoi(env) >= 4 ? 4 : atoi(env) >= 2 ? 2 : 1;
     const int threads = std::max(32, vlps * KM);
-    const size_t smem = (size_t)(2 * KM) * esz + 256 * (size_t)K;
+    const size_t smem = std::max<size_t>((size_t)(2 * KM) * esz, (size_t)kBtBlk) + kBtBlk * (size_t)K;
 #define LHMM_VL(RR, KMV)                                                                         \
   do {                                                                                           \
-    if (vlps == 4) viterbi_large_kernel<RR, KMV, 4><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace); \
-    else if (vlps == 2) viterbi_large_kernel<RR, KMV, 2><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace); \
-    else viterbi_large_kernel<RR, KMV, 1><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace); \
+    RR* lbw = (RR*)((uint8_t*)workspace + align256((size_t)N * K));                              \
+    emission_seq_kernel<RR><<<dim3((unsigned)((max_T + kEmSeqChunk - 1) / kEmSeqChunk), (unsigned)B), 256, 0, st>>>(a, K, lbw); \
+    if (vlps == 4) viterbi_large_kernel<RR, KMV, 4><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace, lbw); \
+    else if (vlps == 2) viterbi_large_kernel<RR, KMV, 2><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace, lbw); \
+    else viterbi_large_kernel<RR, KMV, 1><<<(unsigned)B, threads, smem, st>>>(a, K, (uint8_t*)workspace, lbw); \
   } while (0)
     if (dtype == LOGHMM_F64) {
       if (KM == 16) LHMM_VL(double, 16);

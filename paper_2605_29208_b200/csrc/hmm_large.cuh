@@ -396,10 +396,262 @@ struct SplitWs {
   void* qws;          // [N, K] beta~ (linear, max 1)
   void* wws;          // [N, K] w_t
   double* seg_part;   // [B, kPostSegs, width] per-segment statistics
+  int sparse_ok;      // take the structural-zero sweeps when A allows it (LOGHMM_FBL_SPARSE=0: never)
 };
 constexpr int kPostSegs = 16;
 constexpr int kPostWarps = 8;
 constexpr int kPostPitch = 64 + 4;
+
+// ---------------------------------------------------------------------------
+// Structural zeros in the sweeps (config 5's banded A): a zero A_ij adds
+// nothing to the forward / backward sums, so each state only visits its
+// non-zero sources (forward: column j) or targets (backward: row j).  One warp
+// per sequence and direction, KM / 32 states per lane, the carried vector in
+// shared memory behind a __syncwarp: no CTA barriers, one warp max-reduction
+// per step.  Same recursion and workspace contents as the dense sweeps below
+// (the backward vector is left unnormalised by its own maximum: it stays in
+// [min A, 1], and every consumer is scale-invariant per step).
+// ---------------------------------------------------------------------------
+constexpr int kSweepNZ = 12;  // non-zeros per column / row the sparse sweeps cover
+constexpr int kSweepPB = 16;  // steps of log b fetched ahead per block
+
+template <typename R, int KM, int NZ>
+__device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R* __restrict__ lbws,
+                                                const SplitWs& sw, R* av, bool bwd, int64_t b) {
+  typedef Num<R> N;
+  constexpr int PB = kSweepPB;
+  constexpr int SPL = KM <= 32 ? 1 : KM / 32;  // states per lane
+  const int lane = threadIdx.x;
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  const loghmm_model_t* md = a.model;
+  // lanes past K mirror state 0 and never store
+  const bool act0 = lane < K;
+  bool act[SPL];
+  int js[SPL];
+  const R* src[SPL][NZ];  // &av[source / target index]
+  R Av[SPL][NZ];
+#pragma unroll
+  for (int s = 0; s < SPL; ++s) {
+    js[s] = lane + 32 * s;
+    act[s] = js[s] < K;
+    const int j = act[s] ? js[s] : 0;
+#pragma unroll
+    for (int n = 0; n < NZ; ++n) {
+      src[s][n] = av;
+      Av[s][n] = R(0);
+    }
+    int cnt = 0;
+    for (int i = 0; i < K; ++i) {
+      const R v = (R)(bwd ? md->A[j * K + i] : md->A[i * K + j]);
+      if (act[s] && v > R(0)) {
+#pragma unroll
+        for (int n = 0; n < NZ; ++n)
+          if (n == cnt) {
+            src[s][n] = av + i;
+            Av[s][n] = v;
+          }
+        ++cnt;
+      }
+    }
+  }
+  (void)act0;
+  for (int e = lane; e < KM; e += 32) av[e] = R(0);
+  auto dot = [&](int s) -> R {
+    R c0 = R(0), c1 = R(0), c2 = R(0);
+#pragma unroll
+    for (int n = 0; n < NZ; n += 3) {
+      c0 = fma(Av[s][n], *src[s][n], c0);
+      if (n + 1 < NZ) c1 = fma(Av[s][n + 1], *src[s][n + 1], c1);
+      if (n + 2 < NZ) c2 = fma(Av[s][n + 2], *src[s][n + 2], c2);
+    }
+    return (c0 + c1) + c2;
+  };
+  __syncwarp();
+  const int64_t j0 = act[0] ? js[0] : 0;
+
+  if (!bwd) {
+    // NaN observations (inference.py:117-118): one coalesced scan
+    bool nan_seen = false;
+    {
+      const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
+      const R* y1g = a.n_streams > 1 ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+      for (int t = lane; t < T; t += 32) {
+        const R v0 = y0g[t];
+        const R v1 = y1g ? y1g[t] : R(0);
+        nan_seen |= (v0 != v0) | (v1 != v1);
+      }
+      nan_seen = __any_sync(kFull, nan_seen);
+    }
+    const bool hasA = a.log_alpha != nullptr;
+    R* pA = hasA ? reinterpret_cast<R*>(a.log_alpha) + start * K + j0 : nullptr;  // running row pointers
+    R* pW = reinterpret_cast<R*>(a.alpha_ws) + start * K + j0;
+    const R* pL = lbws + start * K + j0;
+    R lpi[SPL];
+#pragma unroll
+    for (int s = 0; s < SPL; ++s) lpi[s] = act[s] ? (R)md->log_pi[js[s]] : N::ninf();
+    int dead_t = INT_MAX;
+    double lam = 0.0;
+    R lamf = R(0);
+    R a_j[SPL];
+#pragma unroll
+    for (int s = 0; s < SPL; ++s) a_j[s] = R(0);
+    R lbn[PB][SPL];
+#pragma unroll
+    for (int u = 0; u < PB; ++u)
+#pragma unroll
+      for (int s = 0; s < SPL; ++s) lbn[u][s] = (act[s] && u < T) ? pL[(int64_t)u * K + 32 * s] : N::ninf();
+    for (int tb = 0; tb < T; tb += PB) {
+      R lbc[PB][SPL];
+      pL += (int64_t)PB * K;
+#pragma unroll
+      for (int u = 0; u < PB; ++u)
+#pragma unroll
+        for (int s = 0; s < SPL; ++s) {
+          lbc[u][s] = lbn[u][s];
+          lbn[u][s] = (act[s] && tb + PB + u < T) ? pL[(int64_t)u * K + 32 * s] : N::ninf();
+        }
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
+        const int t = tb + u;
+        if (t >= T) break;
+        R uu[SPL];
+        R M = N::ninf();
+#pragma unroll
+        for (int s = 0; s < SPL; ++s) {
+          const R acc = dot(s);
+          const R la_ = t == 0 ? lpi[s] : (acc > R(0) ? N::flog(acc) : N::ninf());
+          uu[s] = act[s] ? la_ + lbc[u][s] : N::ninf();
+          M = rmax(M, uu[s]);
+        }
+        if (hasA) {
+#pragma unroll
+          for (int s = 0; s < SPL; ++s)
+            if (act[s]) pA[32 * s] = lamf + uu[s];
+          pA += K;
+        }
+        M = warp_max(M);
+        if (!(M > N::ninf())) {  // rare: a dead observation (every log b is -inf)?
+          R mlb = N::ninf();
+#pragma unroll
+          for (int s = 0; s < SPL; ++s) mlb = rmax(mlb, lbc[u][s]);
+          mlb = warp_max(mlb);
+          if (!(mlb > N::ninf()) && t < dead_t) dead_t = t;
+        } else {
+          lam += (double)M;
+          lamf = (R)lam;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < SPL; ++s) {
+          a_j[s] = (M > N::ninf()) ? N::fexp(uu[s] - M) : R(0);
+          if (act[s]) {
+            av[js[s]] = a_j[s];
+            pW[32 * s] = a_j[s];
+          }
+        }
+        pW += K;
+        __syncwarp();
+      }
+    }
+    R sm = R(0);
+#pragma unroll
+    for (int s = 0; s < SPL; ++s) sm += act[s] ? a_j[s] : R(0);
+    sm = warp_sum(sm);
+    const double LL = sm > R(0) ? lam + (double)N::flog(sm) : -CUDART_INF;
+    if (lane == 0) {
+      a.ll[b] = LL;
+      if (a.flags) {
+        a.flags[2 * b] = dead_t == INT_MAX ? -1 : dead_t;
+        a.flags[2 * b + 1] = nan_seen ? 1 : 0;
+      }
+    }
+    return;
+  }
+
+  // backward sweep: beta~ (qws), w_t = b~_t beta~_t scaled to max 1 (wws), log beta
+  const bool hasB = a.log_beta != nullptr;
+  const int64_t last = (int64_t)(T - 1) * K;
+  R* pB = hasB ? reinterpret_cast<R*>(a.log_beta) + start * K + j0 + last : nullptr;
+  R* pQ = reinterpret_cast<R*>(sw.qws) + start * K + j0 + last;
+  R* pW = reinterpret_cast<R*>(sw.wws) + start * K + j0 + last;
+  const R* pL = lbws + start * K + j0 + last;
+  R r[SPL];
+#pragma unroll
+  for (int s = 0; s < SPL; ++s) r[s] = R(0);
+  double rho = 0.0;
+  R rhof = R(0);
+  R lbn[PB][SPL];
+#pragma unroll
+  for (int u = 0; u < PB; ++u)
+#pragma unroll
+    for (int s = 0; s < SPL; ++s)
+      lbn[u][s] = (act[s] && T - 1 - u >= 0) ? pL[-(int64_t)u * K + 32 * s] : N::ninf();
+  for (int tb = T - 1; tb >= 0; tb -= PB) {
+    R lbc[PB][SPL];
+    pL -= (int64_t)PB * K;
+#pragma unroll
+    for (int u = 0; u < PB; ++u)
+#pragma unroll
+      for (int s = 0; s < SPL; ++s) {
+        lbc[u][s] = lbn[u][s];
+        lbn[u][s] = (act[s] && tb - PB - u >= 0) ? pL[-(int64_t)u * K + 32 * s] : N::ninf();
+      }
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      const int t = tb - u;
+      if (t < 0) break;
+#pragma unroll
+      for (int s = 0; s < SPL; ++s)
+        if (act[s]) {
+          if (hasB) pB[32 * s] = rhof + r[s];
+          pQ[32 * s] = N::fexp(r[s]);
+        }
+      if (hasB) pB -= K;
+      pQ -= K;
+      if (t == 0) break;
+      R lr[SPL];
+      R M = N::ninf();
+#pragma unroll
+      for (int s = 0; s < SPL; ++s) {
+        lr[s] = act[s] ? lbc[u][s] + r[s] : N::ninf();
+        M = rmax(M, lr[s]);
+      }
+      M = warp_max(M);
+      const bool fin = M > N::ninf();
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < SPL; ++s) {
+        const R w = fin ? N::fexp(lr[s] - M) : R(0);
+        if (act[s]) {
+          av[js[s]] = w;
+          pW[32 * s] = w;
+        }
+      }
+      pW -= K;
+      __syncwarp();
+      if (fin) {
+        rho += (double)M;
+        rhof = (R)rho;
+      }
+#pragma unroll
+      for (int s = 0; s < SPL; ++s) {
+        const R acc = dot(s);
+        r[s] = (act[s] && acc > R(0)) ? N::flog(acc) : N::ninf();
+      }
+    }
+  }
+}
+
+// the smallest instantiated non-zero budget that covers maxnz
+template <typename R, int KM>
+__device__ __forceinline__ void fb_sparse_sweep_nz(const FBArgs& a, int K, const R* __restrict__ lbws,
+                                                   const SplitWs& sw, R* av, bool bwd, int64_t b,
+                                                   int maxnz) {
+  if (maxnz <= 5) fb_sparse_sweep<R, KM, 5>(a, K, lbws, sw, av, bwd, b);
+  else if (maxnz <= 9) fb_sparse_sweep<R, KM, 9>(a, K, lbws, sw, av, bwd, b);
+  else fb_sparse_sweep<R, KM, kSweepNZ>(a, K, lbws, sw, av, bwd, b);
+}
 
 template <typename R, int KM, int P>
 __global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int K,
@@ -418,6 +670,24 @@ __global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int
   const int jt = tid / P;
   const bool bwd = blockIdx.x >= a.B;
   const int64_t b = bwd ? blockIdx.x - a.B : blockIdx.x;
+  // structural sparsity of A: the largest number of non-zeros of a column
+  // (forward) or row (backward)
+  __shared__ int s_maxnz;
+  if (tid == 0) s_maxnz = 0;
+  __syncthreads();
+  if (tid < K) {
+    int cnt = 0;
+    for (int i = 0; i < K; ++i) cnt += (bwd ? a.model->A[tid * K + i] : a.model->A[i * K + tid]) > 0.0 ? 1 : 0;
+    atomicMax(&s_maxnz, cnt);
+  }
+  __syncthreads();
+  // (fp32 only: one warp cannot hide fp64's software exp / log, the dense
+  // sweeps with one state per lane stay faster there)
+  if (sizeof(R) == 4 && s_maxnz <= kSweepNZ && sw.sparse_ok) {
+    if (tid >= 32) return;
+    fb_sparse_sweep_nz<R, KM>(a, K, lbws, sw, av, bwd, b, s_maxnz);
+    return;
+  }
   const int64_t start = a.offsets[b];
   const int T = (int)(a.offsets[b + 1] - start);
   const bool act = jt < K;
@@ -803,6 +1073,251 @@ __global__ void __launch_bounds__(256) fb_fold_kernel(const FBArgs a, int K, con
   }
 }
 
+// Structural zeros (config 5: a banded transition matrix).  A candidate through
+// log A[i][j] = -inf is -inf whatever the score, so it can only be the argmax
+// when every candidate of the column is -inf — and then numpy's argmax returns
+// index 0.  Restricting column j to its finite sources (ascending i, so the
+// first-index rule is kept) and mapping an all -inf column to index 0 is
+// therefore bit-identical to the dense recursion (inference.py:204-207).
+constexpr int kVitNZ = 12;  // finite sources per column the sparse path covers
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One lane per state, KM / 32 warps per sequence (the other warps of the CTA
+// have exited).  Every lane keeps its column's source offsets and log A values
+// in registers, forms the <= kVitNZ candidates from the shared score vector and
+// reduces them with a first-index (value, index) tree.
+// Backtrace over the byte backpointer table bk [T][K] (global workspace), in
+// blocks of kBtBlk rows walking down: the block's rows are copied to shared
+// memory with 16-byte loads (8 in flight per thread; byte loads when K is not
+// a multiple of 16), thread 0 follows the chain through shared memory into a
+// byte stage, and all threads write the int64 path coalesced.
+constexpr int kBtBlk = 256;
+template <typename SyncF>
+__device__ __forceinline__ void backtrace_blocks(const uint8_t* __restrict__ bk, int K, int T,
+                                                 int64_t* __restrict__ path, uint8_t* bblk,
+                                                 uint8_t* pstage, int* s_cur, int tid, int nt,
+                                                 SyncF sync) {
+  for (int hi = T - 1; hi >= 0; hi -= kBtBlk) {
+    const int lo = max(0, hi - kBtBlk + 1);
+    const int rows = hi - lo + 1;
+    const int nbytes = rows * K;
+    const uint8_t* src = bk + (int64_t)lo * K;
+    if ((K & 15) == 0) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+      uint4* d4 = reinterpret_cast<uint4*>(bblk);
+      const int n4 = nbytes >> 4;
+      for (int e0 = tid; e0 < n4; e0 += 8 * nt) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u * nt < n4) v[u] = s4[e0 + u * nt];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u * nt < n4) d4[e0 + u * nt] = v[u];
+      }
+    } else {
+      for (int e0 = tid; e0 < nbytes; e0 += 8 * nt) {
+        uint8_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u * nt < nbytes) v[u] = src[e0 + u * nt];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u * nt < nbytes) bblk[e0 + u * nt] = v[u];
+      }
+    }
+    sync();
+    if (tid == 0) {
+      int c = *s_cur;
+      for (int t = hi; t >= lo; --t) {
+        pstage[t - lo] = (uint8_t)c;
+        if (t >= 1) c = bblk[(t - lo) * K + c];
+      }
+      *s_cur = c;
+    }
+    sync();
+    for (int e = tid; e < rows; e += nt) path[lo + e] = (int64_t)pstage[e];
+    sync();
+  }
+}
+
+constexpr int kVitPB = 16;  // steps of precomputed log b fetched ahead per block
+
+template <typename R, int KM, int NZ>
+__device__ __forceinline__ void viterbi_sparse_path(const VitArgs& a, int K, uint8_t* backws,
+                                                    const R* __restrict__ lbws, R* dvb, uint8_t* bblk,
+                                                    int* s_cur) {
+  typedef Num<R> N;
+  constexpr int PB = kVitPB;
+  static_assert(PB % 2 == 0, "the score buffers alternate with the step parity");
+  constexpr int NT = KM < 32 ? 32 : KM;  // threads taking part
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  const bool act = tid < K;
+  const int j = act ? tid : 0;
+  const loghmm_model_t* md = a.model;
+  int off[NZ];
+  const R* src[NZ];  // &scores[source] in buffer 0 (buffer 1 is KM elements further)
+  R lav[NZ];
+#pragma unroll
+  for (int n = 0; n < NZ; ++n) {
+    off[n] = 0;
+    src[n] = dvb;
+    lav[n] = N::ninf();
+  }
+  {
+    int cnt = 0;
+    for (int i = 0; i < K; ++i) {
+      const R v = (R)md->log_A[i * K + j];
+      if (act && v > N::ninf()) {
+#pragma unroll
+        for (int n = 0; n < NZ; ++n)
+          if (n == cnt) {
+            off[n] = i;
+            src[n] = dvb + i;
+            lav[n] = v;
+          }
+        ++cnt;
+      }
+    }
+  }
+  const R* __restrict__ pL = lbws + start * K + j;  // log b_t[j], running row pointer
+  uint8_t* bk = backws + start * K;
+  auto sync = [&]() {
+    if constexpr (NT == 32) __syncwarp();
+    else named_bar_sync(1, NT);
+  };
+  for (int e = tid; e < 2 * KM; e += NT) dvb[e] = N::ninf();
+  sync();
+  if (act && T > 0) {
+    dvb[j] = N::add((R)md->log_pi[j], pL[0]);
+    bk[j] = 0;
+    if (a.back) a.back[start * K + j] = 0;
+  }
+  sync();
+  uint8_t* pK = bk + K + j;                                            // backpointer row of step 1
+  uint8_t* pX = a.back ? a.back + (start + 1) * K + j : nullptr;       // optional byte table (tests)
+  R* const mine = dvb + j;
+  pL += K;
+  R lbn[PB];  // the next block's emission terms, loaded a block ahead
+#pragma unroll
+  for (int u = 0; u < PB; ++u) lbn[u] = (act && 1 + u < T) ? pL[(int64_t)u * K] : R(0);
+  // step t = tb + u reads score buffer (t - 1) & 1 = u & 1 and writes the other
+  for (int tb = 1; tb < T; tb += PB) {
+    R lbc[PB];
+    pL += (int64_t)PB * K;
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      lbc[u] = lbn[u];
+      lbn[u] = (act && tb + PB + u < T) ? pL[(int64_t)u * K] : R(0);
+    }
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      if (tb + u >= T) break;
+      const int rd = (u & 1) * KM, wr = ((u + 1) & 1) * KM;
+      R cv[NZ];
+      int ci[NZ];
+#pragma unroll
+      for (int n = 0; n < NZ; ++n) {
+        cv[n] = N::add(src[n][rd], lav[n]);
+        ci[n] = off[n];
+      }
+      // first-index argmax tree: the right operand wins only when strictly greater
+#pragma unroll
+      for (int w = 1; w < NZ; w <<= 1) {
+#pragma unroll
+        for (int n = 0; n + w < NZ; n += 2 * w) {
+          const bool r = cv[n + w] > cv[n];
+          cv[n] = r ? cv[n + w] : cv[n];
+          ci[n] = r ? ci[n + w] : ci[n];
+        }
+      }
+      const R best = cv[0];
+      const int bi = best > N::ninf() ? ci[0] : 0;  // an all -inf column: numpy's argmax is 0
+      if (act) {
+        mine[wr] = N::add(best, lbc[u]);
+        *pK = (uint8_t)bi;
+        if (pX) *pX = (uint8_t)bi;
+      }
+      pK += K;
+      if (pX) pX += K;
+      sync();
+    }
+  }
+  const int cur = T > 0 ? (T - 1) & 1 : 0;  // buffer holding the last step's scores
+  if (tid == 0) {
+    const R* dv = dvb + cur * KM;
+    R bv = dv[0];
+    int bi = 0;
+    for (int i = 1; i < K; ++i)
+      if (dv[i] > bv) {
+        bv = dv[i];
+        bi = i;
+      }
+    a.log_joint[b] = (double)bv;
+    *s_cur = bi;
+  }
+  sync();
+  __threadfence_block();
+  backtrace_blocks(bk, K, T, a.path + start, bblk, reinterpret_cast<uint8_t*>(dvb), s_cur, tid, NT, sync);
+}
+
+template <typename R, int KM>
+__device__ __forceinline__ void viterbi_sparse_nz(const VitArgs& a, int K, uint8_t* backws,
+                                                  const R* __restrict__ lbws, R* dvb, uint8_t* bblk,
+                                                  int* s_cur, int maxnz) {
+  if (maxnz <= 5) viterbi_sparse_path<R, KM, 5>(a, K, backws, lbws, dvb, bblk, s_cur);
+  else if (maxnz <= 9) viterbi_sparse_path<R, KM, 9>(a, K, backws, lbws, dvb, bblk, s_cur);
+  else viterbi_sparse_path<R, KM, kVitNZ>(a, K, backws, lbws, dvb, bblk, s_cur);
+}
+
+// Emission log-densities of one batch for the large-K Viterbi (reference-exact,
+// emission_log_matrix: inference.py:93-126), T-parallel: block (chunk, b)
+// covers kEmSeqChunk steps of sequence b, thread (t mod TPB, j) evaluates state
+// j with its parameters in registers and writes coalesced rows.  NaN
+// observations (inference.py:117-118) and log-gamma lookups outside the host
+// table are recorded in the sequence's flag word.
+constexpr int kEmSeqChunk = 1024;
+template <typename R>
+__global__ void __launch_bounds__(256) emission_seq_kernel(const VitArgs a, int K, R* __restrict__ out) {
+  typedef Num<R> N;
+  const int64_t b = blockIdx.y;
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  const int t0 = blockIdx.x * kEmSeqChunk;
+  if (t0 >= T) return;
+  const int t1 = min(T, t0 + kEmSeqChunk);
+  const int TPB = 256 / K;
+  const int tid = threadIdx.x;
+  const int j = tid % K, ts = tid / K;
+  if (ts >= TPB) return;
+  const loghmm_model_t* md = a.model;
+  const bool two = a.n_streams > 1;
+  const loghmm_emission_t e0 = md->em[0][j];
+  loghmm_emission_t e1;
+  if (two) e1 = md->em[1][j];
+  const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  R* o = out + start * K + j;
+  bool oob = false, nan_seen = false;
+  for (int t = t0 + ts; t < t1; t += TPB) {
+    const R v0 = y0g[t];
+    const R v1 = two ? y1g[t] : R(0);
+    nan_seen |= (v0 != v0) | (v1 != v1);
+    R v = exact_logb<R>(e0, v0, a.lut, a.lut_n, oob);
+    if (two) v = N::add(v, exact_logb<R>(e1, v1, a.lut, a.lut_n, oob));
+    o[(int64_t)t * K] = v;
+  }
+  if (a.flags && (nan_seen || oob))
+    atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 2 * b + 1),
+             (unsigned long long)((nan_seen ? 1 : 0) | (oob ? 2 : 0)));
+}
+
 // Viterbi, one CTA per sequence, four lanes per destination state j (the
 // Quarter layout of fb_large_kernel): lane q scans the sources i = q, q + 4,
 // ... with log A[i][j] in registers, and the four partial (max, first index)
@@ -814,18 +1329,35 @@ __global__ void __launch_bounds__(256) fb_fold_kernel(const FBArgs a, int K, con
 // with blocks of backpointer rows prefetched into shared memory.
 template <typename R, int KM, int P>
 __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int K,
-                                                            uint8_t* backws) {
+                                                            uint8_t* backws,
+                                                            const R* __restrict__ lbws) {
   typedef Num<R> N;
   constexpr int NQ = KM / P;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* dvb = reinterpret_cast<R*>(smem_raw);                    // [2][KM] scores
-  uint8_t* bblk = reinterpret_cast<uint8_t*>(dvb + 2 * KM);  // 256*K bytes
+  // [kBtBlk * K] backpointer rows; the score buffers (>= kBtBlk bytes) double as the path stage
+  uint8_t* bblk = smem_raw + (2 * KM * sizeof(R) > kBtBlk ? 2 * KM * sizeof(R) : (size_t)kBtBlk);
   __shared__ int s_cur;
+  __shared__ int s_maxnz;
   const int tid = threadIdx.x;
   const int q = tid & (P - 1);
   const int jt = tid / P;
   const int64_t b = blockIdx.x;
   if (b >= a.B) return;
+  // structural sparsity of log A: the largest number of finite sources of a column
+  if (tid == 0) s_maxnz = 0;
+  __syncthreads();
+  if (tid < K) {
+    int cnt = 0;
+    for (int i = 0; i < K; ++i) cnt += a.model->log_A[i * K + tid] > -CUDART_INF ? 1 : 0;
+    atomicMax(&s_maxnz, cnt);
+  }
+  __syncthreads();
+  if (s_maxnz <= kVitNZ && a.sparse_ok) {
+    if (tid >= (KM < 32 ? 32 : KM)) return;
+    viterbi_sparse_nz<R, KM>(a, K, backws, lbws, dvb, bblk, &s_cur, s_maxnz);
+    return;
+  }
   const int64_t start = a.offsets[b];
   const int T = (int)(a.offsets[b + 1] - start);
   const bool act = jt < K;
@@ -838,64 +1370,60 @@ __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int
     const int i = P * s + q;
     la[s] = (act && i < K) ? (R)md->log_A[i * K + j] : N::ninf();
   }
-  const loghmm_emission_t e0 = md->em[0][j];
-  loghmm_emission_t e1;
-  const bool two = a.n_streams > 1;
-  if (two) e1 = md->em[1][j];
-  const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
-  const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  constexpr int PB = kVitPB;
+  const R* __restrict__ lbj = lbws + start * K + j;  // log b_t[j] at lbj[t * K]
   uint8_t* bk = backws + start * K;
-  bool oob = false, nan_seen = false;
-  auto logb = [&](R v0, R v1) -> R {
-    nan_seen |= (v0 != v0) | (v1 != v1);  // inference.py:117-118 (validate_sequence)
-    R v = exact_logb<R>(e0, v0, a.lut, a.lut_n, oob);
-    if (two) v = N::add(v, exact_logb<R>(e1, v1, a.lut, a.lut_n, oob));
-    return v;
-  };
   for (int e = tid; e < 2 * KM; e += blockDim.x) dvb[e] = N::ninf();
   __syncthreads();
   if (lead && T > 0) {
-    dvb[j] = N::add((R)md->log_pi[j], logb(y0g[0], two ? y1g[0] : R(0)));
+    dvb[j] = N::add((R)md->log_pi[j], lbj[0]);
     bk[j] = 0;
     if (a.back) a.back[start * K + j] = 0;
   }
   __syncthreads();
   int cur = 0;
-  R yn0 = T > 1 ? y0g[1] : R(0), yn1 = (two && T > 1) ? y1g[1] : R(0);
-  for (int t = 1; t < T; ++t) {
-    const R v0 = yn0, v1 = yn1;
-    if (t + 1 < T) {  // prefetch step t + 1
-      yn0 = y0g[t + 1];
-      if (two) yn1 = y1g[t + 1];
-    }
-    const R lb = act ? logb(v0, v1) : R(0);
-    const R* dv = dvb + cur * KM;
-    R best = N::add(dv[q], la[0]);
-    int bi = q;
+  R lbn[PB];  // the next block's emission terms, loaded a block ahead
 #pragma unroll
-    for (int s = 1; s < NQ; ++s) {
-      const R c = N::add(dv[P * s + q], la[s]);
-      if (c > best) {
-        best = c;
-        bi = P * s + q;
-      }
+  for (int u = 0; u < PB; ++u) lbn[u] = (lead && 1 + u < T) ? lbj[(int64_t)(1 + u) * K] : R(0);
+  for (int tb = 1; tb < T; tb += PB) {
+    R lbc[PB];
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      lbc[u] = lbn[u];
+      lbn[u] = (lead && tb + PB + u < T) ? lbj[(int64_t)(tb + PB + u) * K] : R(0);
     }
 #pragma unroll
-    for (int o = 1; o < P; o <<= 1) {
-      const R ov = __shfl_xor_sync(kFull, best, o);
-      const int oi = __shfl_xor_sync(kFull, bi, o);
-      if (ov > best || (ov == best && oi < bi)) {
-        best = ov;
-        bi = oi;
+    for (int u = 0; u < PB; ++u) {
+      const int t = tb + u;
+      if (t >= T) break;
+      const R* dv = dvb + cur * KM;
+      R best = N::add(dv[q], la[0]);
+      int bi = q;
+#pragma unroll
+      for (int s = 1; s < NQ; ++s) {
+        const R c = N::add(dv[P * s + q], la[s]);
+        if (c > best) {
+          best = c;
+          bi = P * s + q;
+        }
       }
+#pragma unroll
+      for (int o = 1; o < P; o <<= 1) {
+        const R ov = __shfl_xor_sync(kFull, best, o);
+        const int oi = __shfl_xor_sync(kFull, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      cur ^= 1;
+      if (lead) {
+        dvb[cur * KM + j] = N::add(best, lbc[u]);
+        bk[(int64_t)t * K + j] = (uint8_t)bi;
+        if (a.back) a.back[(start + t) * K + j] = (uint8_t)bi;
+      }
+      __syncthreads();
     }
-    cur ^= 1;
-    if (lead) {
-      dvb[cur * KM + j] = N::add(best, lb);
-      bk[(int64_t)t * K + j] = (uint8_t)bi;
-      if (a.back) a.back[(start + t) * K + j] = (uint8_t)bi;
-    }
-    __syncthreads();
   }
   if (tid == 0) {
     const R* dv = dvb + cur * KM;
@@ -907,28 +1435,12 @@ __global__ void __launch_bounds__(256) viterbi_large_kernel(const VitArgs a, int
         bi = i;
       }
     a.log_joint[b] = (double)bv;
-    if (a.flags && (nan_seen || oob)) a.flags[2 * b + 1] |= (nan_seen ? 1 : 0) | (oob ? 2 : 0);
     s_cur = bi;
   }
   __syncthreads();
   __threadfence_block();
-  // backtrace in blocks of 256 rows, walking down
-  constexpr int BLK = 256;
-  for (int hi = T - 1; hi >= 0; hi -= BLK) {
-    const int lo = max(0, hi - BLK + 1);
-    const int rows = hi - lo + 1;
-    for (int e = tid; e < rows * K; e += blockDim.x) bblk[e] = bk[(int64_t)lo * K + e];
-    __syncthreads();
-    if (tid == 0) {
-      int c = s_cur;
-      for (int t = hi; t >= lo; --t) {
-        a.path[start + t] = c;
-        if (t >= 1) c = bblk[(t - lo) * K + c];
-      }
-      s_cur = c;
-    }
-    __syncthreads();
-  }
+  backtrace_blocks(bk, K, T, a.path + start, bblk, reinterpret_cast<uint8_t*>(dvb), &s_cur, tid,
+                   (int)blockDim.x, [] { __syncthreads(); });
 }
 
 }  // namespace lhmm

@@ -41,6 +41,7 @@ struct VitArgs {
   int64_t plane_words;  // per warp (= max_T * NP rounded)
   int warp_smem_words;  // shared words per warp
   int64_t* flags;
+  int sparse_ok;  // large K: take the structural-zero path when log A allows it
 };
 
 

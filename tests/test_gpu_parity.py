@@ -656,6 +656,110 @@ def test_large_k_viterbi_exact_ties(K, dtype):
         assert np.array_equal(vit.back[s].cpu().numpy().astype(np.int64), bk)
 
 
+def _banded_model(rng, K, half, tie=False, dead_first=False):
+    """Banded transitions (structural zeros outside |i - j| <= half), BASELINE
+    config 5's shape.  tie: constant band values and repeated rates, so
+    candidates tie exactly; dead_first: pi puts all mass on the last state, so
+    the low states stay unreachable (-inf scores) for the first steps and some
+    columns see only -inf candidates (numpy's argmax then returns index 0)."""
+    A = np.zeros((K, K))
+    for i in range(K):
+        lo, hi = max(0, i - half), min(K, i + half + 1)
+        A[i, lo:hi] = 1.0 if tie else rng.dirichlet(np.ones(hi - lo)) * 0.2
+        if not tie:
+            A[i, i] += 0.8
+    A /= A.sum(1, keepdims=True)
+    pi = np.zeros(K)
+    if dead_first:
+        pi[K - 1 if dead_first is True else int(dead_first)] = 1.0
+    else:
+        pi[:] = 1.0 / K
+    rates = [2.0 + (k % 3) for k in range(K)] if tie else list(0.5 * (np.arange(K) + 1))
+    return H.HmmModel(pi, A, tuple(H.Poisson(float(r)) for r in rates))
+
+
+@pytest.mark.parametrize("K", [12, 33, 64])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("variant", ["band", "ties", "dead"])
+@pytest.mark.parametrize("sparse", ["1", "0"])
+def test_large_k_viterbi_banded_structural_zeros(K, dtype, variant, sparse, monkeypatch):
+    """K > 8 Viterbi on a banded transition matrix: the structural-zero path
+    (finite sources only, an all -inf column mapped to index 0) and the dense
+    path give the reference's path, backpointers and log joint bit for bit,
+    including exact ties inside the band and columns whose candidates are all
+    -inf."""
+    monkeypatch.setenv("LOGHMM_VL_SPARSE", sparse)
+    rng = np.random.default_rng(1300 + K)
+    m = _banded_model(rng, K, 4, tie=variant == "ties", dead_first=variant == "dead")
+    seqs = [rng.poisson(6.0, n).astype(float) for n in (1, 2, 40, 700)]
+    lp, la = O.model_tables(m.initial, m.transitions)
+    vit = H.viterbi_batch(m, seqs, dtype=dtype, back=True)
+    R = np.float32 if dtype == "float32" else np.float64
+    for b, y in enumerate(seqs):
+        lb = O.emission_matrix(to_tuples(m), y.astype(R), R)
+        with np.errstate(invalid="ignore"):
+            p, j, bk = O.viterbi(lp.astype(R), la.astype(R), lb, R)
+        s = slice(vit.offsets[b], vit.offsets[b + 1])
+        assert np.array_equal(vit.path[s].cpu().numpy(), p), (K, b)
+        assert np.array_equal(vit.back[s].cpu().numpy().astype(np.int64), bk), (K, b)
+        assert vit.log_joint[b].item() == j
+
+
+@pytest.mark.parametrize("K", [12, 33, 64])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("variant", ["band", "dead"])
+@pytest.mark.parametrize("sparse", ["1", "0"])
+def test_large_k_banded_forward_backward(K, dtype, variant, sparse, monkeypatch):
+    """K > 8 forward-backward on a banded transition matrix, through the
+    structural-zero sweeps and through the dense ones: LL, log alpha / log
+    beta, gamma, per-step xi and one Baum-Welch iteration against the oracle
+    (states that are unreachable for the first steps included)."""
+    monkeypatch.setenv("LOGHMM_FBL_SPARSE", sparse)
+    rng = np.random.default_rng(1700 + K)
+    # "dead": all initial mass on one state near the data's rate, so the far
+    # states are unreachable (-inf) for the first steps.  (A start that is
+    # also wildly inconsistent with the data puts alpha~ and beta~ more than
+    # fp32's exponent range apart; that case is exercised in fp64 by the
+    # Viterbi test above and documented as an fp32 range limit in DESIGN.md.)
+    m = _banded_model(rng, K, 4, dead_first=min(K - 1, 11) if variant == "dead" else False)
+    seqs = [rng.poisson(6.0, n).astype(float) for n in (1, 2, 17, 40, 700)]
+    r = H.posteriors_batch(m, seqs, dtype=dtype, include_xi=True)
+    with np.errstate(divide="ignore"):
+        lp, la = O.model_tables(m.initial, m.transitions)
+    f64 = dtype == "float64"
+    tol = 1e-9 if f64 else 1e-5
+    X_ = r.xi.cpu().numpy().astype(np.float64)
+    for b, y in enumerate(seqs):
+        with np.errstate(invalid="ignore", divide="ignore"):
+            o = O.posteriors(lp, la, O.emission_matrix(to_tuples(m), y), include_xi=True)
+        s = slice(r.offsets[b], r.offsets[b + 1])
+        xs = slice(r.offsets[b] - b, r.offsets[b + 1] - b - 1)
+        assert r.log_likelihood[b].item() == pytest.approx(o["ll"], rel=1e-9 if f64 else 1e-4)
+        np.testing.assert_allclose(r.gamma[s].double().cpu().numpy(), o["gamma"], atol=tol)
+        for ours, ref in ((r.log_alpha, o["log_alpha"]), (r.log_beta, o["log_beta"])):
+            mine = ours[s].double().cpu().numpy()
+            fin = np.isfinite(ref)
+            if f64:
+                assert np.array_equal(np.isfinite(mine), fin)
+            else:
+                # the fp32 recursions carry max-normalised linear vectors: entries more
+                # than ~87 nats below the step's maximum flush to log 0 = -inf
+                assert not np.isfinite(mine[~fin]).any()
+                lost = fin & ~np.isfinite(mine)
+                rowmax = np.where(fin, ref, -np.inf).max(axis=1, keepdims=True)
+                assert (np.broadcast_to(rowmax, ref.shape)[lost] - ref[lost] > 80.0).all()
+                # (entries within a few nats of that edge are fp32 denormals: compared loosely)
+                fin = fin & np.isfinite(mine) & (rowmax - np.where(fin, ref, -np.inf) < 80.0)
+            np.testing.assert_allclose(mine[fin], ref[fin], rtol=1e-9 if f64 else 1e-5, atol=tol if f64 else 2e-4)
+        if len(y) > 1:
+            np.testing.assert_allclose(X_[xs], o["xi"], atol=tol)
+    fitted, rep = H.baum_welch(m, seqs, H.TrainingConfig(max_iterations=2, rel_tol=1e-300), dtype=dtype)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        pi2, A2, em2, trace, _, _ = O.baum_welch(m.initial, m.transitions, to_tuples(m), seqs, 2)
+    np.testing.assert_allclose(rep.log_likelihood_trace, trace, rtol=1e-9 if f64 else 1e-4)
+    np.testing.assert_allclose(fitted.transitions, A2, atol=1e-9 if f64 else 1e-4)
+
+
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_error_semantics_equal_length_batches(dtype):
     """Error paths of the equal-length decomposition (chunk operators + meet in
