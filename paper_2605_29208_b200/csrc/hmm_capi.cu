@@ -276,6 +276,18 @@ static cudaError_t launch_split(const FBArgs& a, int K, int KM, int lps, int64_t
     return cudaErrorInvalidValue;
   const unsigned hz = (K > 32) ? (unsigned)PostGeom<R>::H : 1u;
   fb_post_kernel<R><<<dim3(kPostSegs, (unsigned)B, hz), 32 * kPostWarps, psm, st>>>(a, K, sw);
+  // structurally sparse A: the dense kernel above returns at once and one of
+  // these takes the pass (each checks the row non-zero count on the device)
+  {
+    auto ssm = [](int nz) {
+      return (size_t)kPostWarps * 64 * sizeof(R) +
+             (size_t)(2 * 64 * LOGHMM_NSLOT + 2 * 64 + 64 * nz) * sizeof(double);
+    };
+    const dim3 pg(kPostSegs, (unsigned)B);
+    fb_post_sparse_kernel<R, 5><<<pg, 32 * kPostWarps, ssm(5), st>>>(a, K, sw);
+    fb_post_sparse_kernel<R, 9><<<pg, 32 * kPostWarps, ssm(9), st>>>(a, K, sw);
+    fb_post_sparse_kernel<R, kPostNZ><<<pg, 32 * kPostWarps, ssm(kPostNZ), st>>>(a, K, sw);
+  }
   if (fold) fb_fold_kernel<<<(unsigned)B, 256, 0, st>>>(a, K, sw);
   return cudaGetLastError();
 }

@@ -429,6 +429,17 @@ __device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// Z = X Y by rows (Z[r] = sum_i X[r][i] Y[i]): packed FFMA2 for fp32, even K
+template <typename R, int K>
+__device__ __forceinline__ void matmul_rows(const R (&X)[K][K], const R (&Y)[K][K], R (&Z)[K][K]) {
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    V<R, K>::mul_s(Z[r], X[r][0], Y[0]);
+#pragma unroll
+    for (int i = 1; i < K; ++i) V<R, K>::fma_s(Z[r], X[r][i], Y[i], Z[r]);
+  }
+}
+
 constexpr int kFbcWarps = 4;  // warps (sequences) per CTA: one warpgroup
 
 // Power-of-two normalisation of a scan operator (FMNMX max; exponent kept in
@@ -451,8 +462,16 @@ __device__ __forceinline__ void norm_op(R (&Z)[K][K], double& off2) {
   }
 }
 
+// LHMM_FBC_MAXNREG (Makefile: FBC_MAXREG) caps the kernel's registers instead
+// of bounding the block size, e.g. 160 so that a one-warp Viterbi CTA fits
+// beside three FB CTAs in an SM's register file.
+#ifdef LHMM_FBC_MAXNREG
+#define LHMM_FBC_BOUNDS __maxnreg__(LHMM_FBC_MAXNREG)
+#else
+#define LHMM_FBC_BOUNDS __launch_bounds__(128)
+#endif
 template <typename R, int K, int CFG>
-__global__ void __launch_bounds__(128)
+__global__ void LHMM_FBC_BOUNDS
     fb_chunk_kernel(const FBCArgs a) {
   typedef Num<R> N;
   typedef CfgTraits<CFG> TR;
@@ -723,7 +742,7 @@ __global__ void __launch_bounds__(128)
         shfl_mat<R, K>(P, po, Q, qo, d, true);
         if (lane >= d) {
           R Z[K][K];
-          matmul<R, K>(P, Q, Z);
+          matmul_rows<R, K>(P, Q, Z);
 #pragma unroll
           for (int r = 0; r < K; ++r)
 #pragma unroll
@@ -779,7 +798,7 @@ __global__ void __launch_bounds__(128)
         shfl_mat<R, K>(Y, yo, S, so, d, false);
         if (lane + d < kWarp) {
           R Z[K][K];
-          matmul<R, K>(S, Y, Z);
+          matmul_rows<R, K>(S, Y, Z);
 #pragma unroll
           for (int r = 0; r < K; ++r)
 #pragma unroll

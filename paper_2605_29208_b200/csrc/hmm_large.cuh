@@ -854,6 +854,24 @@ __device__ __forceinline__ R row_dot64(const R* __restrict__ row, const R* __res
   return (c[0] + c[1]) + (c[2] + c[3]);
 }
 
+// Largest number of non-zeros of a row of A (counted by the CTA's first K
+// threads): both post kernels below evaluate it, exactly one of them runs.
+__device__ __forceinline__ int cta_row_maxnz(const loghmm_model_t* md, int K, int* s_val) {
+  if (threadIdx.x == 0) *s_val = 0;
+  __syncthreads();
+  if ((int)threadIdx.x < K) {
+    int cnt = 0;
+    for (int i = 0; i < K; ++i) cnt += md->A[threadIdx.x * K + i] > 0.0 ? 1 : 0;
+    atomicMax(s_val, cnt);
+  }
+  __syncthreads();
+  return *s_val;
+}
+constexpr int kPostNZ = 12;
+__device__ __forceinline__ bool post_takes_sparse(const FBArgs& a, const SplitWs& sw, int maxnz) {
+  return sw.sparse_ok && a.xi == nullptr && maxnz <= kPostNZ;
+}
+
 // T-parallel pass: CTA (seg, b) takes steps [seg*len, (seg+1)*len) of
 // sequence b in chunks of TC steps.  Phase 1, one warp per step (lane l owns
 // states l and l + 32): gamma_t and the statistics, and for xi the row
@@ -875,13 +893,15 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) fb_post_kernel(co
   R* Tw = Ta + TC * 64;                    // [TC][64] w_t
   double* sts = reinterpret_cast<double*>(Tw + TC * 64);  // [2][64][NSLOT] + [2][64]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const loghmm_model_t* md = a.model;
+  __shared__ int s_maxnz;
+  if (post_takes_sparse(a, sw, cta_row_maxnz(md, K, &s_maxnz))) return;  // fb_post_sparse_kernel's launch
   const int64_t b = blockIdx.y;
   const int seg = blockIdx.x;
   const int64_t start = a.offsets[b];
   const int T = (int)(a.offsets[b + 1] - start);
   const int len = (T + kPostSegs - 1) / kPostSegs;
   const int t0 = seg * len, t1 = min(T, t0 + len);
-  const loghmm_model_t* md = a.model;
   for (int e = tid; e < 64 * 64; e += blockDim.x) {
     const int r = e >> 6, c = e & 63;
     As[r * PITCH + c] = (r < K && c < K) ? (R)md->A[r * K + c] : R(0);
@@ -1050,6 +1070,186 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) fb_post_kernel(co
       const int i = 4 * ti + r, jj = 4 * tj + c;
       if (i < K && jj < K) row[i * K + jj] = (double)X[r][c];
     }
+  for (int jj = tid; jj < K; jj += blockDim.x) {
+    row[K * K + jj] = gts[jj];
+    row[K * K + K + jj] = gts[64 + jj];
+    for (int v = 0; v < 2; ++v)
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq)
+        row[K * K + 2 * K + (v * K + jj) * LOGHMM_NSLOT + qq] = sts[(v * 64 + jj) * LOGHMM_NSLOT + qq];
+  }
+}
+
+// T-parallel pass for a structurally sparse A (config 5's band): same segment
+// decomposition and statistics as fb_post_kernel, but a zero A_ij carries no
+// xi mass, so lane i keeps only the xi sums of its row's non-zero targets in
+// registers (no shared tiles, no rank-TC phase) and q = A w is a sparse dot.
+template <typename R, int NZ>
+__global__ void __launch_bounds__(256, 2) fb_post_sparse_kernel(const FBArgs a, int K, const SplitWs sw) {
+  typedef Num<R> N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* wv = reinterpret_cast<R*>(smem_raw);                               // [warps][64] w_t
+  double* sts = reinterpret_cast<double*>(wv + kPostWarps * 64);        // [2][64][NSLOT] + [2][64]
+  double* xfold = sts + 2 * 64 * LOGHMM_NSLOT + 2 * 64;                 // [64][NZ]
+  __shared__ int s_maxnz;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const loghmm_model_t* md = a.model;
+  const int maxnz = cta_row_maxnz(md, K, &s_maxnz);
+  if (!post_takes_sparse(a, sw, maxnz) || maxnz > NZ || (NZ > 5 && maxnz <= 5) || (NZ > 9 && maxnz <= 9)) return;
+  const int64_t b = blockIdx.y;
+  const int seg = blockIdx.x;
+  const int64_t start = a.offsets[b];
+  const int T = (int)(a.offsets[b + 1] - start);
+  const int len = (T + kPostSegs - 1) / kPostSegs;
+  const int t0 = seg * len, t1 = min(T, t0 + len);
+  const bool two = a.n_streams > 1;
+  int is[2];
+  bool act[2];
+  EmP<R> p0[2], p1[2];
+  int tgt[2][NZ];
+  R Ar[2][NZ], xs[2][NZ];
+  R* mw = wv + wid * 64;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    is[s] = lane + 32 * s;
+    act[s] = is[s] < K;
+    const int ii = act[s] ? is[s] : 0;
+    p0[s] = load_emission<R>(md->em[0][ii]);
+    if (two) p1[s] = load_emission<R>(md->em[1][ii]);
+    else p1[s].fam = LOGHMM_FAM_NONE;
+#pragma unroll
+    for (int n = 0; n < NZ; ++n) {
+      tgt[s][n] = 0;
+      Ar[s][n] = R(0);
+      xs[s][n] = R(0);
+    }
+    int cnt = 0;
+    for (int jj = 0; jj < K; ++jj) {
+      const R v = (R)md->A[ii * K + jj];
+      if (act[s] && v > R(0)) {
+#pragma unroll
+        for (int n = 0; n < NZ; ++n)
+          if (n == cnt) {
+            tgt[s][n] = jj;
+            Ar[s][n] = v;
+          }
+        ++cnt;
+      }
+    }
+  }
+  const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
+  const R* y1g = two ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
+  const R* aws = reinterpret_cast<const R*>(a.alpha_ws) + start * K;
+  const R* qws = reinterpret_cast<const R*>(sw.qws) + start * K;
+  const R* wws = reinterpret_cast<const R*>(sw.wws) + start * K;
+  R* outG = a.gamma ? reinterpret_cast<R*>(a.gamma) + start * K : nullptr;
+  R st[2][2][LOGHMM_NSLOT];
+  R gtot[2] = {R(0), R(0)}, g0[2] = {R(0), R(0)};
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    for (int v = 0; v < 2; ++v)
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][v][qq] = R(0);
+  // this step's inputs are loaded one step ahead (the next step's loads are in
+  // flight while the current one is reduced)
+  R nat[2], nqe[2], nap[2], nwj[2], ny0 = R(0), ny1 = R(0);
+  auto fetch = [&](int t) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const bool ok = act[s] && t < t1;
+      nat[s] = ok ? aws[(int64_t)t * K + is[s]] : R(0);
+      nqe[s] = ok ? qws[(int64_t)t * K + is[s]] : R(0);
+      nap[s] = (ok && t >= 1) ? aws[(int64_t)(t - 1) * K + is[s]] : R(0);
+      nwj[s] = (ok && t >= 1) ? wws[(int64_t)t * K + is[s]] : R(0);
+    }
+    ny0 = t < t1 ? y0g[t] : R(0);
+    ny1 = (two && t < t1) ? y1g[t] : R(0);
+  };
+  fetch(t0 + wid);
+  for (int t = t0 + wid; t < t1; t += kPostWarps) {
+    R at[2], qe[2], ap[2], wj[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      at[s] = nat[s];
+      qe[s] = nqe[s];
+      ap[s] = nap[s];
+      wj[s] = nwj[s];
+    }
+    const R yv0 = ny0, yv1 = ny1;
+    fetch(t + kPostWarps);
+    const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (!act[s]) continue;
+      const R gj = at[s] * qe[s] / gz;
+      if (outG) outG[(int64_t)t * K + is[s]] = gj;
+      ObsFeat<R> f0, f1;
+      stat_features<R>(f0, yv0, p0[s].fam);
+      if (two) stat_features<R>(f1, yv1, p1[s].fam);
+      R accs[LOGHMM_NSLOT];
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][0][qq];
+      stat_acc_rt<R>(accs, gj, p0[s], f0);
+      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][0][qq] = accs[qq];
+      if (two) {
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][1][qq];
+        stat_acc_rt<R>(accs, gj, p1[s], f1);
+        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][1][qq] = accs[qq];
+      }
+      if (t < T - 1) gtot[s] += gj;
+      if (t == 0) g0[s] = gj;
+    }
+    if (t == 0) continue;
+    // xi_{t-1}: q_i = (A w_t)_i over the row's non-zeros, Z = alpha~_{t-1} . q
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      if (act[s]) mw[is[s]] = wj[s];
+    __syncwarp();
+    R qv[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      R acc = R(0);
+#pragma unroll
+      for (int n = 0; n < NZ; ++n) acc = fma(Ar[s][n], mw[tgt[s][n]], acc);
+      qv[s] = acc;
+    }
+    const R Z = warp_sum(ap[0] * qv[0] + ap[1] * qv[1]);
+    const R iz = R(1) / Z;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const R ta = ap[s] * iz;
+#pragma unroll
+      for (int n = 0; n < NZ; ++n) xs[s][n] = fma(ta, mw[tgt[s][n]], xs[s][n]);
+    }
+  }
+  // fold the statistics and the xi sums over the warps in order
+  double* gts = sts + 2 * 64 * LOGHMM_NSLOT;  // [2][64]: gamma totals, first gamma
+  for (int e = tid; e < 2 * 64 * LOGHMM_NSLOT + 2 * 64 + 64 * NZ; e += blockDim.x) sts[e] = 0.0;
+  __syncthreads();
+  for (int w = 0; w < kPostWarps; ++w) {
+    if (wid == w) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        for (int v = 0; v < 2; ++v)
+          for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) sts[(v * 64 + is[s]) * LOGHMM_NSLOT + qq] += (double)st[s][v][qq];
+        gts[is[s]] += (double)gtot[s];
+        gts[64 + is[s]] += (double)g0[s];
+#pragma unroll
+        for (int n = 0; n < NZ; ++n) xfold[is[s] * NZ + n] += (double)xs[s][n];
+      }
+    }
+    __syncthreads();
+  }
+  double* row = sw.seg_part + ((int64_t)b * kPostSegs + seg) * a.stats_width;
+  for (int e = tid; e < K * K; e += blockDim.x) row[e] = 0.0;
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      if (act[s]) {
+#pragma unroll
+        for (int n = 0; n < NZ; ++n)
+          if (Ar[s][n] > R(0)) row[is[s] * K + tgt[s][n]] = xfold[is[s] * NZ + n];
+      }
+  }
   for (int jj = tid; jj < K; jj += blockDim.x) {
     row[K * K + jj] = gts[jj];
     row[K * K + K + jj] = gts[64 + jj];
