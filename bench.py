@@ -336,6 +336,25 @@ def _kernel_times(p, flush, n):
     return statistics.mean(kfb), statistics.mean(kvit)
 
 
+def _fb_alone_ms(p, flush, n):
+    """Mean duration of the forward-backward call launched alone (no concurrent
+    Viterbi kernel on the SMs), L2 flushed before each launch."""
+    import torch
+
+    from paper_2605_29208_b200 import engine
+
+    ts = []
+    for i in range(n):
+        flush.fill_(i & 0xFF)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        engine.forward_backward(p.batch, p.dm, stats=True, out=p.fb, workspace=p.ws_fb)
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    return statistics.mean(ts)
+
+
 def _fb_name(K, td_is_f32, T):
     import torch  # noqa: F401
 
@@ -391,6 +410,7 @@ def ours(a):
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
         fb_ms, vit_ms = _kernel_times(p, flush, min(a.steps, 10))
+        fb_alone_ms = _fb_alone_ms(p, flush, min(a.steps, 10))
         step_ms = sum(ts) / len(ts)
         t_local = torch.tensor([step_ms], device="cuda", dtype=torch.float64)
         if pg is not None:
@@ -410,6 +430,10 @@ def ours(a):
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "alg_bytes_per_launch": fb_bytes, "kernel_ms": fb_ms,
+                # the same launch with the SMs to itself (inside the step it shares
+                # them with the concurrent Viterbi kernel)
+                "kernel_alone_ms": fb_alone_ms,
+                "frac_alone": fb_bytes / (fb_alone_ms / 1000.0) / 1e9 / peak,
             },
             "pipeline_roofline": {
                 "bytes_per_step_M1": m1_bytes, "achieved_gbs": m1_bytes / (step_ms / 1000.0) / 1e9,

@@ -136,12 +136,16 @@ static cudaError_t dispatch_fb_small(int K, const FBArgs& a, int cfg, bool gl, d
 }
 
 // Chain-warp Viterbi (hmm_viterbi3.cuh; K in [2,4], sequences whose
-// backpointer bytes fit in shared memory).  LOGHMM_VIT_ALGO=lanes forces the
-// K-lanes-per-sequence kernel; LOGHMM_VIT_NW picks 8 or 16 warps per CTA.
+// backpointer bytes fit in shared memory), selected with LOGHMM_VIT_ALGO=chain;
+// LOGHMM_VIT_NW picks 8 or 16 warps per CTA.  Alone it is the faster kernel at
+// 16 warps (66 vs 70 us at config 2), but inside the step, next to the
+// forward-backward kernel, the K-lanes-per-sequence kernel issues fewer
+// instructions in total (16M vs 24M warp-instructions) and the step is bound
+// by issue slots: 135 vs 139 us.  So the K-lane kernel stays the default.
 static bool vit3_ok(int K, int esz, int64_t max_T, int* nw, size_t* smem) {
   if (K < 2 || K > 4) return false;
   const char* env = getenv("LOGHMM_VIT_ALGO");
-  if (env && strcmp(env, "lanes") == 0) return false;
+  if (!env || strcmp(env, "chain") != 0) return false;
   const size_t bytes = v3_smem_bytes(esz, max_T);
   if (bytes > 200 * 1024) return false;
   *smem = bytes;

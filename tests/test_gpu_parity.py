@@ -138,10 +138,10 @@ def _random_gauss_model(rng, K):
                                    for _ in range(K)))
 
 
-@pytest.fixture(params=["auto", "lanes"])
+@pytest.fixture(params=["auto", "chain"])
 def vit_algo(request, monkeypatch):
-    """Run a test under both Viterbi layouts (the chain-warp kernel for
-    K <= 4 by default, K lanes per sequence on request)."""
+    """Run a test under both Viterbi layouts (K lanes per sequence by default,
+    the chain-warp kernel for K <= 4 on request)."""
     if request.param != "auto":
         monkeypatch.setenv("LOGHMM_VIT_ALGO", request.param)
     else:

@@ -6,8 +6,6 @@ run() {
   python3 -c "import json; d=json.loads(open('gpurun_out/pm_$1.json').read().strip().splitlines()[-1]); print('$1', round(d['ms_per_step']*1e3,1), round(d['roofline']['kernel_ms']*1e3,1), round(d['pipeline_roofline']['viterbi_kernel_ms']*1e3,1))"
 }
 LOGHMM_VIT_ALGO=lanes run lanes
-LOGHMM_VIT_ALGO=lanes LOGHMM_VIT_WPB=2 run lanes_wpb2
-LOGHMM_VIT_ALGO=lanes LOGHMM_VIT_WPB=1 run lanes_wpb1
-LOGHMM_VIT_NW=8 run nw8
-LOGHMM_VIT_NW=16 run nw16
-LOGHMM_PIPE_ORDER=serial LOGHMM_VIT_NW=16 run nw16_serial
+LOGHMM_VIT_ALGO=chain LOGHMM_VIT_NW=8 run nw8
+LOGHMM_VIT_ALGO=chain LOGHMM_VIT_NW=16 run nw16
+LOGHMM_PIPE_ORDER=serial LOGHMM_VIT_ALGO=chain LOGHMM_VIT_NW=16 run nw16_serial

@@ -4,9 +4,9 @@ mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "viterbi or Viterbi" -p no:cacheprovider > gpurun_out/pytest_vit.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_vit.log
 tail -5 gpurun_out/pytest_vit.log
 for nw in 8 16; do
-  LOGHMM_VIT_NW=$nw timeout 300 python tools/prof_kernels.py --dtype float32 --only vit > gpurun_out/prof_vit_f32_nw$nw.json 2>&1
-  LOGHMM_VIT_NW=$nw timeout 300 python tools/prof_kernels.py --dtype float64 --only vit > gpurun_out/prof_vit_f64_nw$nw.json 2>&1
-  LOGHMM_VIT_NW=$nw timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench_nw$nw.json 2> gpurun_out/bench_nw$nw.err
+  LOGHMM_VIT_ALGO=chain LOGHMM_VIT_NW=$nw timeout 300 python tools/prof_kernels.py --dtype float32 --only vit > gpurun_out/prof_vit_f32_nw$nw.json 2>&1
+  LOGHMM_VIT_ALGO=chain LOGHMM_VIT_NW=$nw timeout 300 python tools/prof_kernels.py --dtype float64 --only vit > gpurun_out/prof_vit_f64_nw$nw.json 2>&1
+  LOGHMM_VIT_ALGO=chain LOGHMM_VIT_NW=$nw timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench_nw$nw.json 2> gpurun_out/bench_nw$nw.err
 done
 LOGHMM_VIT_ALGO=lanes timeout 300 python tools/prof_kernels.py --dtype float32 --only vit > gpurun_out/prof_vit_f32_lanes.json 2>&1
 LOGHMM_VIT_ALGO=lanes timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench_lanes.json 2> gpurun_out/bench_lanes.err
