@@ -22,6 +22,13 @@ KEYS = [
     ("sm__inst_executed_pipe_xu.sum", "mufu_xu_instructions"),
     ("sm__inst_executed_pipe_fp64.sum", "fp64_instructions"),
     ("lts__t_bytes.sum", "l2_bytes"),
+    ("smsp__inst_executed.sum", "warp_instructions_smsp"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_pct"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "pipe_fma_pct"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "pipe_alu_pct"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "pipe_xu_mufu_pct"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "pipe_fp64_pct"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "pipe_lsu_pct"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
 ]
