@@ -136,20 +136,27 @@ static cudaError_t dispatch_fb_small(int K, const FBArgs& a, int cfg, bool gl, d
 }
 
 // Chain-warp Viterbi (hmm_viterbi3.cuh; K in [2,4], sequences whose
-// backpointer bytes fit in shared memory), selected with LOGHMM_VIT_ALGO=chain;
-// LOGHMM_VIT_NW picks 8 or 16 warps per CTA.  Alone it is the faster kernel at
-// 16 warps (66 vs 70 us at config 2), but inside the step, next to the
-// forward-backward kernel, the K-lanes-per-sequence kernel issues fewer
-// instructions in total (16M vs 24M warp-instructions) and the step is bound
-// by issue slots: 135 vs 139 us.  So the K-lane kernel stays the default.
-static bool vit3_ok(int K, int esz, int64_t max_T, int* nw, size_t* smem) {
+// backpointer bytes fit in shared memory).  LOGHMM_VIT_ALGO = chain | lanes
+// forces a layout, LOGHMM_VIT_NW picks 8 or 16 warps per CTA.  Default:
+// * Gaussian / Poisson emissions (a handful of IEEE operations): the
+//   K-lanes-per-sequence kernel.  Alone the chain-warp kernel is the faster
+//   one at 16 warps (66 vs 70 us at config 2), but inside the step, next to
+//   the forward-backward kernel, the two issue about the same number of
+//   instructions and the step is bound by issue slots: 135 vs 139 us.
+// * families whose exact density calls log1p / log / cos (Student-t, Gamma,
+//   von Mises, joint, mixed): the chain-warp kernel, 16 warps — its helper
+//   warps evaluate the densities T-parallel, while the K-lane kernel
+//   evaluates them inside the sequential recursion (config 3: 1.14 ms).
+static bool vit3_ok(int K, int esz, int64_t max_T, int cfg, int* nw, size_t* smem) {
   if (K < 2 || K > 4) return false;
   const char* env = getenv("LOGHMM_VIT_ALGO");
-  if (!env || strcmp(env, "chain") != 0) return false;
+  const bool cheap = cfg == kCfgGauss || cfg == kCfgPoisson;
+  if (env && strcmp(env, "lanes") == 0) return false;
+  if (!(env && strcmp(env, "chain") == 0) && cheap) return false;
   const size_t bytes = v3_smem_bytes(esz, max_T);
   if (bytes > 200 * 1024) return false;
   *smem = bytes;
-  *nw = 8;
+  *nw = cheap ? 8 : 16;
   if (const char* e2 = getenv("LOGHMM_VIT_NW")) *nw = atoi(e2) >= 16 ? 16 : 8;
   return true;
 }
@@ -508,9 +515,10 @@ int32_t loghmm_viterbi(int32_t dtype, const loghmm_model_t* h_desc, const loghmm
   cudaError_t e;
   int v3_nw = 0;
   size_t v3_smem = 0;
-  if (vit3_ok(K, dtype == LOGHMM_F64 ? 8 : 4, max_T, &v3_nw, &v3_smem)) {
-    int fams = 0;
-    const int cfg = cfg_of(h_desc, &fams);
+  int fams0 = 0;
+  const int cfg0 = cfg_of(h_desc, &fams0);
+  if (vit3_ok(K, dtype == LOGHMM_F64 ? 8 : 4, max_T, cfg0, &v3_nw, &v3_smem)) {
+    const int cfg = cfg0;
     dim3 grid((unsigned)((B + kV3Seq - 1) / kV3Seq));
     e = dtype == LOGHMM_F64 ? dispatch_vit3<double>(K, a, cfg, v3_nw, grid, v3_smem, st)
                             : dispatch_vit3<float>(K, a, cfg, v3_nw, grid, v3_smem, st);
@@ -719,9 +727,9 @@ static int32_t guard_launch(int32_t dtype, loghmm_model_t* model_out, const void
                                                          K, stream_index, guard_state,
                                                          n_candidates, part);
   if (sums) {
-    guard_fold_kernel<<<1, 64, 0, st>>>(K, stream_index, guard_state, n_candidates, part, nblocks, sums);
+    guard_fold_kernel<<<1, kGuardSelThreads, 0, st>>>(K, stream_index, guard_state, n_candidates, part, nblocks, sums);
   } else {
-    guard_select_kernel<<<1, 64, 0, st>>>(model_out, K, stream_index, guard_state, n_candidates,
+    guard_select_kernel<<<1, kGuardSelThreads, 0, st>>>(model_out, K, stream_index, guard_state, n_candidates,
                                           part, nblocks, status, need_more);
   }
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
@@ -774,7 +782,7 @@ int32_t loghmm_student_guard_select(loghmm_model_t* model_out, int32_t K, int32_
   if (!model_out || !guard_state || !sums || !status || !need_more || K < 1 ||
       K > LOGHMM_MAX_STATES || n_candidates < 2 || n_candidates > LOGHMM_GUARD_CANDIDATES)
     return LOGHMM_EINVAL;
-  guard_select_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(model_out, K, stream_index, guard_state,
+  guard_select_kernel<<<1, kGuardSelThreads, 0, (cudaStream_t)stream>>>(model_out, K, stream_index, guard_state,
                                                           n_candidates, sums, 1, status, need_more);
   return cudaGetLastError() == cudaSuccess ? LOGHMM_OK : LOGHMM_ELAUNCH;
 }

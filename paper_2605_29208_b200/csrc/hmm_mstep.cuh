@@ -598,20 +598,47 @@ __device__ inline double st_ll(double n, double sum_l1p, double sigma, double nu
   return n * c - (nu + 1.0) / 2.0 * sum_l1p;
 }
 
-__global__ void guard_select_kernel(loghmm_model_t* __restrict__ mout, int K, int sidx,
-                                    double* __restrict__ guard, int ncand,
-                                    const double* __restrict__ part, int nblocks,
-                                    int32_t* __restrict__ status, int* __restrict__ need_more) {
+// Sum of the per-block partials of (state j, candidate k) in block order (the
+// fixed order that makes the guard's decision reproducible): the loads of 16
+// blocks are issued together, the additions stay sequential.
+__device__ inline double guard_partial_sum(const double* __restrict__ part, int nblocks, int K, int j,
+                                           int k) {
+  double s = 0.0;
+  const double* p = part + (size_t)j * LOGHMM_GUARD_CANDIDATES + k;
+  const size_t stride = (size_t)K * LOGHMM_GUARD_CANDIDATES;
+  int blk = 0;
+  for (; blk + 16 <= nblocks; blk += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = p[(size_t)(blk + u) * stride];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s += v[u];
+  }
+  for (; blk < nblocks; ++blk) s += p[(size_t)blk * stride];
+  return s;
+}
+
+// (launched with one block of kGuardSelThreads threads: the (state, candidate)
+// sums are formed in parallel, then thread j decides for state j)
+constexpr int kGuardSelThreads = 256;
+__global__ void __launch_bounds__(kGuardSelThreads)
+    guard_select_kernel(loghmm_model_t* __restrict__ mout, int K, int sidx,
+                        double* __restrict__ guard, int ncand,
+                        const double* __restrict__ part, int nblocks,
+                        int32_t* __restrict__ status, int* __restrict__ need_more) {
+  __shared__ double s_sums[LOGHMM_MAX_STATES * LOGHMM_GUARD_CANDIDATES];
+  for (int pr = threadIdx.x; pr < K * LOGHMM_GUARD_CANDIDATES; pr += blockDim.x) {
+    const int jj = pr / LOGHMM_GUARD_CANDIDATES, k = pr % LOGHMM_GUARD_CANDIDATES;
+    const bool pending = guard[(size_t)(sidx * K + jj) * kGuardStride + 5] != 0.0;
+    s_sums[pr] = (pending && k < ncand) ? guard_partial_sum(part, nblocks, K, jj, k) : 0.0;
+  }
+  __syncthreads();
   const int j = threadIdx.x;
   if (j >= K) return;
   double* gs = guard + (size_t)(sidx * K + j) * kGuardStride;
   if (gs[5] == 0.0) return;
   double sums[LOGHMM_GUARD_CANDIDATES];
-  for (int k = 0; k < ncand; ++k) {
-    double s = 0.0;
-    for (int blk = 0; blk < nblocks; ++blk) s += part[((size_t)blk * K + j) * LOGHMM_GUARD_CANDIDATES + k];
-    sums[k] = s;
-  }
+  for (int k = 0; k < ncand; ++k) sums[k] = s_sums[j * LOGHMM_GUARD_CANDIDATES + k];
   const double mu = gs[0], sigma = gs[1], nu0 = gs[2], n = gs[4];
   const double base = st_ll(n, sums[0], sigma, nu0);
   double c = gs[3];
@@ -761,14 +788,10 @@ __global__ void variance_finish_kernel(loghmm_model_t* __restrict__ mout, int K,
 __global__ void guard_fold_kernel(int K, int sidx, const double* __restrict__ guard, int ncand,
                                   const double* __restrict__ part, int nblocks,
                                   double* __restrict__ sums) {
-  const int j = threadIdx.x;
-  if (j >= K) return;
-  const bool pending = guard[(size_t)(sidx * K + j) * kGuardStride + 5] != 0.0;
-  for (int k = 0; k < LOGHMM_GUARD_CANDIDATES; ++k) {
-    double acc = 0.0;
-    if (pending && k < ncand)
-      for (int blk = 0; blk < nblocks; ++blk) acc += part[((size_t)blk * K + j) * LOGHMM_GUARD_CANDIDATES + k];
-    sums[(size_t)j * LOGHMM_GUARD_CANDIDATES + k] = acc;
+  for (int pr = threadIdx.x; pr < K * LOGHMM_GUARD_CANDIDATES; pr += blockDim.x) {
+    const int j = pr / LOGHMM_GUARD_CANDIDATES, k = pr % LOGHMM_GUARD_CANDIDATES;
+    const bool pending = guard[(size_t)(sidx * K + j) * kGuardStride + 5] != 0.0;
+    sums[pr] = (pending && k < ncand) ? guard_partial_sum(part, nblocks, K, j, k) : 0.0;
   }
 }
 

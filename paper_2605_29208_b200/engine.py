@@ -478,12 +478,19 @@ def student_guard_select(dm_out: DeviceModel, stream_index: int, n_candidates: i
                                             _stream()), "loghmm_student_guard_select")
 
 
-# Candidate batches of the ECME guard: the first launch evaluates the base and
-# GUARD_CANDIDATES-1 halvings, each further launch the next GUARD_CANDIDATES-1;
-# the reference tries at most 60 halvings (distributions.py:1083), so this
-# many launches always reach a decision (a launch with nothing pending exits
-# at once).  Used where the host cannot poll need_more (CUDA graph capture).
-GUARD_LAUNCHES = -(-60 // (_native.GUARD_CANDIDATES - 1))
+# Candidate batches of the ECME guard, as training.baum_welch issues them: the
+# first launch evaluates the base and the first candidate (almost always
+# accepted, so the common case is one cheap data pass), each further launch
+# the next GUARD_CANDIDATES-1 halvings; the reference tries at most 60
+# (distributions.py:1083), so this many launches always reach a decision (a
+# launch with nothing pending exits at once).  Used where the host cannot
+# poll need_more (CUDA graph capture).
+GUARD_FIRST = 2
+GUARD_LAUNCHES = 1 + -(-(60 - (GUARD_FIRST - 1)) // (_native.GUARD_CANDIDATES - 1))
+
+
+def guard_candidates(launch_index: int) -> int:
+    return GUARD_FIRST if launch_index == 0 else _native.GUARD_CANDIDATES
 
 
 def ext_fit(batch: Batch, dm_out: DeviceModel, gamma: torch.Tensor, stream_index: int,

@@ -184,17 +184,16 @@ class Pipeline:
         # batch with no pending state exits at once); training.baum_welch polls
         # need_more instead, with identical results
         for s in self.student_streams:
-            for _ in range(engine.GUARD_LAUNCHES):
+            for i in range(engine.GUARD_LAUNCHES):
+                ncand = engine.guard_candidates(i)
                 if self.pg is None:
                     engine.student_guard(self.batch, self.dm_next, self.fb.gamma, s,
-                                         _native.GUARD_CANDIDATES, self.guard, self.status,
-                                         self.need_more)
+                                         ncand, self.guard, self.status, self.need_more)
                 else:
                     engine.student_guard_partial(self.batch, self.dm_next, self.fb.gamma, s,
-                                                 _native.GUARD_CANDIDATES, self.guard,
-                                                 self.guard_sums)
+                                                 ncand, self.guard, self.guard_sums)
                     self._all_reduce(self.guard_sums)
-                    engine.student_guard_select(self.dm_next, s, _native.GUARD_CANDIDATES,
+                    engine.student_guard_select(self.dm_next, s, ncand,
                                                 self.guard, self.guard_sums, self.status,
                                                 self.need_more)
 

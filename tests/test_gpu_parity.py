@@ -138,10 +138,11 @@ def _random_gauss_model(rng, K):
                                    for _ in range(K)))
 
 
-@pytest.fixture(params=["auto", "chain"])
+@pytest.fixture(params=["auto", "chain", "lanes"])
 def vit_algo(request, monkeypatch):
-    """Run a test under both Viterbi layouts (K lanes per sequence by default,
-    the chain-warp kernel for K <= 4 on request)."""
+    """Run a test under every Viterbi layout: the automatic choice (K lanes per
+    sequence for Gaussian / Poisson, the chain-warp kernel for the families
+    with transcendental densities at K <= 4) and each layout forced."""
     if request.param != "auto":
         monkeypatch.setenv("LOGHMM_VIT_ALGO", request.param)
     else:
