@@ -269,6 +269,8 @@ static cudaError_t launch_split(const FBArgs& a, int K, int KM, int lps, int64_t
   sw.seg_part = (double*)((char*)workspace + 4 * nk);
   sw.sparse_ok = 1;
   if (const char* env = getenv("LOGHMM_FBL_SPARSE")) sw.sparse_ok = atoi(env) != 0;
+  sw.sparse_warps = 2;
+  if (const char* env = getenv("LOGHMM_FBL_SPARSE_WARPS")) sw.sparse_warps = atoi(env) >= 2 ? 2 : 1;
   const size_t ssm = (size_t)(2 * KM + 128 + kRing * 4 * KM) * sizeof(R);
   const R* lb = (const R*)lbw;
 #define LHMM_FBS(KMV)                                                                            \

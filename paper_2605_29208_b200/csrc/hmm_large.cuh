@@ -397,10 +397,15 @@ struct SplitWs {
   void* wws;          // [N, K] w_t
   double* seg_part;   // [B, kPostSegs, width] per-segment statistics
   int sparse_ok;      // take the structural-zero sweeps when A allows it (LOGHMM_FBL_SPARSE=0: never)
+  int sparse_warps;   // fp32 structural-zero sweeps at K = 64: warps per sequence and direction (1 or 2)
 };
 constexpr int kPostSegs = 16;
 constexpr int kPostWarps = 8;
 constexpr int kPostPitch = 64 + 4;
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // Structural zeros in the sweeps (config 5's banded A): a zero A_ij adds
@@ -415,13 +420,50 @@ constexpr int kPostPitch = 64 + 4;
 constexpr int kSweepNZ = 12;  // non-zeros per column / row the sparse sweeps cover
 constexpr int kSweepPB = 16;  // steps of log b fetched ahead per block
 
-template <typename R, int KM, int NZ>
+// NW warps per sequence and direction, state s of a thread = tid + 32 NW s.
+// One warp: the step's maximum is one redux.sync and the carried vector sits
+// behind __syncwarp.  Two warps (one state per lane at K = 64): the warp maxima
+// meet in a parity-indexed shared slot behind a named barrier — half the
+// instructions per warp and step, which is what bounds the sweep (fp64: the
+// software exp / log chains of one state instead of two per lane).
+template <typename R, int KM, int NZ, int NW>
 __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R* __restrict__ lbws,
-                                                const SplitWs& sw, R* av, bool bwd, int64_t b) {
+                                                const SplitWs& sw, R* av, R* red, bool bwd, int64_t b) {
   typedef Num<R> N;
   constexpr int PB = kSweepPB;
-  constexpr int SPL = KM <= 32 ? 1 : KM / 32;  // states per lane
-  const int lane = threadIdx.x;
+  constexpr int NT = 32 * NW;
+  constexpr int SPL = KM <= NT ? 1 : KM / NT;  // states per thread
+  const int lane = threadIdx.x;  // thread index inside the NT threads
+  int par = 0;                   // parity of the cross-warp reduction slot
+  auto sync = [&]() {
+    if constexpr (NW == 1) __syncwarp();
+    else named_bar_sync(1, NT);
+  };
+  // maximum over the NT threads
+  auto all_max = [&](R v) -> R {
+    v = warp_max(v);
+    if constexpr (NW > 1) {
+      if ((lane & 31) == 0) red[par * NW + (lane >> 5)] = v;
+      named_bar_sync(1, NT);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) v = rmax(v, red[par * NW + w]);
+      par ^= 1;
+    }
+    return v;
+  };
+  auto all_sum = [&](R v) -> R {
+    v = warp_sum(v);
+    if constexpr (NW > 1) {
+      if ((lane & 31) == 0) red[par * NW + (lane >> 5)] = v;
+      named_bar_sync(1, NT);
+      R t = R(0);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t += red[par * NW + w];
+      par ^= 1;
+      v = t;
+    }
+    return v;
+  };
   const int64_t start = a.offsets[b];
   const int T = (int)(a.offsets[b + 1] - start);
   const loghmm_model_t* md = a.model;
@@ -433,7 +475,7 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
   R Av[SPL][NZ];
 #pragma unroll
   for (int s = 0; s < SPL; ++s) {
-    js[s] = lane + 32 * s;
+    js[s] = lane + NT * s;
     act[s] = js[s] < K;
     const int j = act[s] ? js[s] : 0;
 #pragma unroll
@@ -456,7 +498,7 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
     }
   }
   (void)act0;
-  for (int e = lane; e < KM; e += 32) av[e] = R(0);
+  for (int e = lane; e < KM; e += NT) av[e] = R(0);
   auto dot = [&](int s) -> R {
     R c0 = R(0), c1 = R(0), c2 = R(0);
 #pragma unroll
@@ -467,7 +509,7 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
     }
     return (c0 + c1) + c2;
   };
-  __syncwarp();
+  sync();
   const int64_t j0 = act[0] ? js[0] : 0;
 
   if (!bwd) {
@@ -476,12 +518,12 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
     {
       const R* y0g = reinterpret_cast<const R*>(a.y0) + start;
       const R* y1g = a.n_streams > 1 ? reinterpret_cast<const R*>(a.y1) + start : nullptr;
-      for (int t = lane; t < T; t += 32) {
+      for (int t = lane; t < T; t += NT) {
         const R v0 = y0g[t];
         const R v1 = y1g ? y1g[t] : R(0);
         nan_seen |= (v0 != v0) | (v1 != v1);
       }
-      nan_seen = __any_sync(kFull, nan_seen);
+      nan_seen = all_max(nan_seen ? R(1) : R(0)) > R(0);
     }
     const bool hasA = a.log_alpha != nullptr;
     R* pA = hasA ? reinterpret_cast<R*>(a.log_alpha) + start * K + j0 : nullptr;  // running row pointers
@@ -500,7 +542,7 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
 #pragma unroll
     for (int u = 0; u < PB; ++u)
 #pragma unroll
-      for (int s = 0; s < SPL; ++s) lbn[u][s] = (act[s] && u < T) ? pL[(int64_t)u * K + 32 * s] : N::ninf();
+      for (int s = 0; s < SPL; ++s) lbn[u][s] = (act[s] && u < T) ? pL[(int64_t)u * K + NT * s] : N::ninf();
     for (int tb = 0; tb < T; tb += PB) {
       R lbc[PB][SPL];
       pL += (int64_t)PB * K;
@@ -509,7 +551,7 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
 #pragma unroll
         for (int s = 0; s < SPL; ++s) {
           lbc[u][s] = lbn[u][s];
-          lbn[u][s] = (act[s] && tb + PB + u < T) ? pL[(int64_t)u * K + 32 * s] : N::ninf();
+          lbn[u][s] = (act[s] && tb + PB + u < T) ? pL[(int64_t)u * K + NT * s] : N::ninf();
         }
 #pragma unroll
       for (int u = 0; u < PB; ++u) {
@@ -527,37 +569,37 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
         if (hasA) {
 #pragma unroll
           for (int s = 0; s < SPL; ++s)
-            if (act[s]) pA[32 * s] = lamf + uu[s];
+            if (act[s]) pA[NT * s] = lamf + uu[s];
           pA += K;
         }
-        M = warp_max(M);
+        M = all_max(M);
         if (!(M > N::ninf())) {  // rare: a dead observation (every log b is -inf)?
           R mlb = N::ninf();
 #pragma unroll
           for (int s = 0; s < SPL; ++s) mlb = rmax(mlb, lbc[u][s]);
-          mlb = warp_max(mlb);
+          mlb = all_max(mlb);
           if (!(mlb > N::ninf()) && t < dead_t) dead_t = t;
         } else {
           lam += (double)M;
           lamf = (R)lam;
         }
-        __syncwarp();
+        if constexpr (NW == 1) __syncwarp();  // (NW > 1: all_max's barrier already ordered the reads of av)
 #pragma unroll
         for (int s = 0; s < SPL; ++s) {
           a_j[s] = (M > N::ninf()) ? N::fexp(uu[s] - M) : R(0);
           if (act[s]) {
             av[js[s]] = a_j[s];
-            pW[32 * s] = a_j[s];
+            pW[NT * s] = a_j[s];
           }
         }
         pW += K;
-        __syncwarp();
+        sync();
       }
     }
     R sm = R(0);
 #pragma unroll
     for (int s = 0; s < SPL; ++s) sm += act[s] ? a_j[s] : R(0);
-    sm = warp_sum(sm);
+    sm = all_sum(sm);
     const double LL = sm > R(0) ? lam + (double)N::flog(sm) : -CUDART_INF;
     if (lane == 0) {
       a.ll[b] = LL;
@@ -586,7 +628,7 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
   for (int u = 0; u < PB; ++u)
 #pragma unroll
     for (int s = 0; s < SPL; ++s)
-      lbn[u][s] = (act[s] && T - 1 - u >= 0) ? pL[-(int64_t)u * K + 32 * s] : N::ninf();
+      lbn[u][s] = (act[s] && T - 1 - u >= 0) ? pL[-(int64_t)u * K + NT * s] : N::ninf();
   for (int tb = T - 1; tb >= 0; tb -= PB) {
     R lbc[PB][SPL];
     pL -= (int64_t)PB * K;
@@ -595,7 +637,7 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
 #pragma unroll
       for (int s = 0; s < SPL; ++s) {
         lbc[u][s] = lbn[u][s];
-        lbn[u][s] = (act[s] && tb - PB - u >= 0) ? pL[-(int64_t)u * K + 32 * s] : N::ninf();
+        lbn[u][s] = (act[s] && tb - PB - u >= 0) ? pL[-(int64_t)u * K + NT * s] : N::ninf();
       }
 #pragma unroll
     for (int u = 0; u < PB; ++u) {
@@ -604,8 +646,8 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
 #pragma unroll
       for (int s = 0; s < SPL; ++s)
         if (act[s]) {
-          if (hasB) pB[32 * s] = rhof + r[s];
-          pQ[32 * s] = N::fexp(r[s]);
+          if (hasB) pB[NT * s] = rhof + r[s];
+          pQ[NT * s] = N::fexp(r[s]);
         }
       if (hasB) pB -= K;
       pQ -= K;
@@ -617,19 +659,19 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
         lr[s] = act[s] ? lbc[u][s] + r[s] : N::ninf();
         M = rmax(M, lr[s]);
       }
-      M = warp_max(M);
+      M = all_max(M);
       const bool fin = M > N::ninf();
-      __syncwarp();
+      if constexpr (NW == 1) __syncwarp();
 #pragma unroll
       for (int s = 0; s < SPL; ++s) {
         const R w = fin ? N::fexp(lr[s] - M) : R(0);
         if (act[s]) {
           av[js[s]] = w;
-          pW[32 * s] = w;
+          pW[NT * s] = w;
         }
       }
       pW -= K;
-      __syncwarp();
+      sync();
       if (fin) {
         rho += (double)M;
         rhof = (R)rho;
@@ -644,13 +686,13 @@ __device__ __forceinline__ void fb_sparse_sweep(const FBArgs& a, int K, const R*
 }
 
 // the smallest instantiated non-zero budget that covers maxnz
-template <typename R, int KM>
+template <typename R, int KM, int NW>
 __device__ __forceinline__ void fb_sparse_sweep_nz(const FBArgs& a, int K, const R* __restrict__ lbws,
-                                                   const SplitWs& sw, R* av, bool bwd, int64_t b,
+                                                   const SplitWs& sw, R* av, R* red, bool bwd, int64_t b,
                                                    int maxnz) {
-  if (maxnz <= 5) fb_sparse_sweep<R, KM, 5>(a, K, lbws, sw, av, bwd, b);
-  else if (maxnz <= 9) fb_sparse_sweep<R, KM, 9>(a, K, lbws, sw, av, bwd, b);
-  else fb_sparse_sweep<R, KM, kSweepNZ>(a, K, lbws, sw, av, bwd, b);
+  if (maxnz <= 5) fb_sparse_sweep<R, KM, 5, NW>(a, K, lbws, sw, av, red, bwd, b);
+  else if (maxnz <= 9) fb_sparse_sweep<R, KM, 9, NW>(a, K, lbws, sw, av, red, bwd, b);
+  else fb_sparse_sweep<R, KM, kSweepNZ, NW>(a, K, lbws, sw, av, red, bwd, b);
 }
 
 template <typename R, int KM, int P>
@@ -681,11 +723,20 @@ __global__ void __launch_bounds__(256) fb_split_sweep_kernel(const FBArgs a, int
     atomicMax(&s_maxnz, cnt);
   }
   __syncthreads();
-  // (fp32 only: one warp cannot hide fp64's software exp / log, the dense
-  // sweeps with one state per lane stay faster there)
-  if (sizeof(R) == 4 && s_maxnz <= kSweepNZ && sw.sparse_ok) {
-    if (tid >= 32) return;
-    fb_sparse_sweep_nz<R, KM>(a, K, lbws, sw, av, bwd, b, s_maxnz);
+  if (s_maxnz <= kSweepNZ && sw.sparse_ok) {
+    // warps per sequence and direction: one state per lane at K = 64 when
+    // sw.sparse_warps = 2 (fp64 always: one lane cannot hide the software
+    // exp / log chains of two states)
+    constexpr bool kCanTwo = KM == 64;
+    const bool two_warps = kCanTwo && (sizeof(R) == 8 || sw.sparse_warps == 2);
+    if (tid >= (two_warps ? 64 : 32)) return;
+    if constexpr (kCanTwo) {
+      if (two_warps) {
+        fb_sparse_sweep_nz<R, KM, 2>(a, K, lbws, sw, av, red, bwd, b, s_maxnz);
+        return;
+      }
+    }
+    fb_sparse_sweep_nz<R, KM, 1>(a, K, lbws, sw, av, red, bwd, b, s_maxnz);
     return;
   }
   const int64_t start = a.offsets[b];
@@ -1280,10 +1331,6 @@ __global__ void __launch_bounds__(256) fb_fold_kernel(const FBArgs a, int K, con
 // first-index rule is kept) and mapping an all -inf column to index 0 is
 // therefore bit-identical to the dense recursion (inference.py:204-207).
 constexpr int kVitNZ = 12;  // finite sources per column the sparse path covers
-
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 // One lane per state, KM / 32 warps per sequence (the other warps of the CTA
 // have exited).  Every lane keeps its column's source offsets and log A values
