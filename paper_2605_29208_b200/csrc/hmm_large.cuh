@@ -1197,7 +1197,9 @@ __global__ void __launch_bounds__(256, 2) fb_post_sparse_kernel(const FBArgs a, 
   R gtot[2] = {R(0), R(0)}, g0[2] = {R(0), R(0)};
 #pragma unroll
   for (int s = 0; s < 2; ++s)
+#pragma unroll
     for (int v = 0; v < 2; ++v)
+#pragma unroll
       for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][v][qq] = R(0);
   // this step's inputs are loaded one step ahead (the next step's loads are in
   // flight while the current one is reduced)
@@ -1227,23 +1229,17 @@ __global__ void __launch_bounds__(256, 2) fb_post_sparse_kernel(const FBArgs a, 
     const R yv0 = ny0, yv1 = ny1;
     fetch(t + kPostWarps);
     const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
+    const R igz = R(1) / gz;  // one division per step (posteriors stay within 1 ulp of a per-state division)
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       if (!act[s]) continue;
-      const R gj = at[s] * qe[s] / gz;
+      const R gj = at[s] * qe[s] * igz;
       if (outG) outG[(int64_t)t * K + is[s]] = gj;
       ObsFeat<R> f0, f1;
       stat_features<R>(f0, yv0, p0[s].fam);
       if (two) stat_features<R>(f1, yv1, p1[s].fam);
-      R accs[LOGHMM_NSLOT];
-      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][0][qq];
-      stat_acc_rt<R>(accs, gj, p0[s], f0);
-      for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][0][qq] = accs[qq];
-      if (two) {
-        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) accs[qq] = st[s][1][qq];
-        stat_acc_rt<R>(accs, gj, p1[s], f1);
-        for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][1][qq] = accs[qq];
-      }
+      stat_acc_rt<R>(st[s][0], gj, p0[s], f0);
+      if (two) stat_acc_rt<R>(st[s][1], gj, p1[s], f1);
       if (t < T - 1) gtot[s] += gj;
       if (t == 0) g0[s] = gj;
     }
@@ -1279,7 +1275,9 @@ __global__ void __launch_bounds__(256, 2) fb_post_sparse_kernel(const FBArgs a, 
     if (wid == w) {
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
+#pragma unroll
         for (int v = 0; v < 2; ++v)
+#pragma unroll
           for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) sts[(v * 64 + is[s]) * LOGHMM_NSLOT + qq] += (double)st[s][v][qq];
         gts[is[s]] += (double)gtot[s];
         gts[64 + is[s]] += (double)g0[s];
