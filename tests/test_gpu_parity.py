@@ -684,6 +684,20 @@ def _banded_model(rng, K, half, tie=False, dead_first=False):
 @pytest.mark.parametrize("variant", ["band", "ties", "dead"])
 @pytest.mark.parametrize("sparse", ["1", "0"])
 def test_large_k_viterbi_banded_structural_zeros(K, dtype, variant, sparse, monkeypatch):
+    _check_banded_viterbi(K, 4, dtype, variant, sparse, monkeypatch)
+
+
+@pytest.mark.parametrize("half", [2, 5, 6])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_large_k_banded_other_bandwidths(half, dtype, monkeypatch):
+    """Band half-widths 2, 5 and 6 (5, 11 and 13 non-zeros per column): the
+    5- and 12-entry instantiations of the structural-zero kernels, and a band
+    just too wide for them (falls back to the dense kernels)."""
+    _check_banded_viterbi(40, half, dtype, "ties", "1", monkeypatch)
+    _check_banded_fb(40, half, dtype, "band", "1", monkeypatch)
+
+
+def _check_banded_viterbi(K, half, dtype, variant, sparse, monkeypatch):
     """K > 8 Viterbi on a banded transition matrix: the structural-zero path
     (finite sources only, an all -inf column mapped to index 0) and the dense
     path give the reference's path, backpointers and log joint bit for bit,
@@ -691,7 +705,7 @@ def test_large_k_viterbi_banded_structural_zeros(K, dtype, variant, sparse, monk
     -inf."""
     monkeypatch.setenv("LOGHMM_VL_SPARSE", sparse)
     rng = np.random.default_rng(1300 + K)
-    m = _banded_model(rng, K, 4, tie=variant == "ties", dead_first=variant == "dead")
+    m = _banded_model(rng, K, half, tie=variant == "ties", dead_first=variant == "dead")
     seqs = [rng.poisson(6.0, n).astype(float) for n in (1, 2, 40, 700)]
     lp, la = O.model_tables(m.initial, m.transitions)
     vit = H.viterbi_batch(m, seqs, dtype=dtype, back=True)
@@ -711,6 +725,10 @@ def test_large_k_viterbi_banded_structural_zeros(K, dtype, variant, sparse, monk
 @pytest.mark.parametrize("variant", ["band", "dead"])
 @pytest.mark.parametrize("sparse", ["1", "0"])
 def test_large_k_banded_forward_backward(K, dtype, variant, sparse, monkeypatch):
+    _check_banded_fb(K, 4, dtype, variant, sparse, monkeypatch)
+
+
+def _check_banded_fb(K, half, dtype, variant, sparse, monkeypatch):
     """K > 8 forward-backward on a banded transition matrix, through the
     structural-zero sweeps and through the dense ones: LL, log alpha / log
     beta, gamma, per-step xi and one Baum-Welch iteration against the oracle
@@ -722,7 +740,7 @@ def test_large_k_banded_forward_backward(K, dtype, variant, sparse, monkeypatch)
     # also wildly inconsistent with the data puts alpha~ and beta~ more than
     # fp32's exponent range apart; that case is exercised in fp64 by the
     # Viterbi test above and documented as an fp32 range limit in DESIGN.md.)
-    m = _banded_model(rng, K, 4, dead_first=min(K - 1, 11) if variant == "dead" else False)
+    m = _banded_model(rng, K, half, dead_first=min(K - 1, 11) if variant == "dead" else False)
     seqs = [rng.poisson(6.0, n).astype(float) for n in (1, 2, 17, 40, 700)]
     r = H.posteriors_batch(m, seqs, dtype=dtype, include_xi=True)
     with np.errstate(divide="ignore"):
