@@ -92,6 +92,16 @@ class Pipeline:
             raise NotImplementedError("multi-rank steps support the five hot-path families only")
         self.s_copy = torch.cuda.Stream(device=dev)
         self._slices = {}
+        # Launch order of the two concurrent kernels.  Viterbi first by default:
+        # its grid is one partial wave, the forward-backward CTAs queued after
+        # it fill the remaining SM slots.  fp64 with K <= 8 and Gaussian /
+        # Poisson emissions is the exception (measured, config 2: 684 vs 778 us
+        # per step): the fp64 forward-backward kernel holds two 255-register
+        # CTAs per SM for 3.5 waves, and the K-lane Viterbi CTAs slot in as those
+        # retire instead of halving the forward-backward occupancy from the start.
+        cheap = all(int(fams[s, j]) in (_native.FAM["gaussian"], _native.FAM["poisson"])
+                    for s in range(self.ns) for j in range(K))
+        self.default_order = "fb_first" if (self.td == torch.float64 and K <= 8 and cheap) else "vit_first"
         # per-kernel CUDA events (recorded on the stream each kernel runs on)
         self.ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for k in ("fb", "vit")}
@@ -117,11 +127,9 @@ class Pipeline:
         main = torch.cuda.current_stream(self.dev)
         self.s_fb.wait_stream(main)
         self.s_vit.wait_stream(main)
-        # Viterbi first by default: its grid is one partial wave (one CTA per
-        # SM), so the forward-backward CTAs queued after it fill the remaining
-        # SM slots and the two kernels run concurrently.
-        # LOGHMM_PIPE_ORDER=fb_first | serial reorders them (measurement aid).
-        order = os.environ.get("LOGHMM_PIPE_ORDER", "vit_first")
+        # (see default_order; LOGHMM_PIPE_ORDER = vit_first | fb_first | serial
+        # overrides it, a measurement aid)
+        order = os.environ.get("LOGHMM_PIPE_ORDER", self.default_order)
 
         def launch_vit():
             with torch.cuda.stream(self.s_vit):
