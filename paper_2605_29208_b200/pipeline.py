@@ -79,7 +79,9 @@ class Pipeline:
         self.ws_vit = engine.Workspace()
         self.ws_red = engine.Workspace()
         self.s_fb = torch.cuda.Stream(device=dev)
-        self.s_vit = torch.cuda.Stream(device=dev)
+        # LOGHMM_VIT_PRIO=1: Viterbi on a high-priority stream (pending Viterbi CTAs
+        # are placed before pending forward-backward CTAs when an SM slot frees)
+        self.s_vit = torch.cuda.Stream(device=dev, priority=-1 if os.environ.get("LOGHMM_VIT_PRIO") == "1" else 0)
         fams = self.dm.host["em"]["family"]
         self.student_streams = sorted({s for s in range(self.ns) for j in range(K)
                                        if int(fams[s, j]) == _native.FAM["student_t"]})
@@ -147,6 +149,10 @@ class Pipeline:
                                         workspace=self.ws_fb)
                 if time_kernels:
                     self.ev["fb"][1].record(self.s_fb)
+                # the statistics reduction and the M-step depend on the
+                # forward-backward kernel only: they follow it on its stream and
+                # overlap whatever is left of the Viterbi kernel
+                self._tail()
 
         if order == "fb_first":
             launch_fb()
@@ -160,7 +166,6 @@ class Pipeline:
             launch_fb()
         main.wait_stream(self.s_fb)
         main.wait_stream(self.s_vit)
-        self._tail()
 
     def _tail(self) -> None:
         """Statistics reduction (+ all-reduce across ranks), M-step and the
