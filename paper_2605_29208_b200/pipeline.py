@@ -280,10 +280,13 @@ class Pipeline:
             self.s_fb.wait_event(ev)
             with torch.cuda.stream(self.s_fb):
                 engine.forward_backward(batch, self.dm, stats=True, out=fb, workspace=self.ws_fb)
+        # reduction + M-step behind the last slice's forward-backward kernel on
+        # its stream (they overlap the last slice's Viterbi kernel)
+        with torch.cuda.stream(self.s_fb):
+            self._tail()
         main.wait_stream(self.s_copy)
         main.wait_stream(self.s_fb)
         main.wait_stream(self.s_vit)
-        self._tail()
 
     def _world(self) -> int:
         import torch.distributed as dist
