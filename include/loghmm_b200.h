@@ -134,7 +134,10 @@ int64_t loghmm_stats_width(int32_t K, int32_t n_streams);
  *                 (training.py:189-194; inference.py:165 for LL = -inf)
  *   flags[2b+1] = bit 0: NaN observation seen (inference.py:117-118)
  *                 bit 1: a log-gamma lookup fell outside the host table
- *                        (Poisson value not bit-exact to math.lgamma)     */
+ *                        (Poisson value not bit-exact to math.lgamma)
+ *                 bit 2: (K > 8) a posterior step's alpha~ . beta~ or alpha~^T A w underflowed
+ *                        the compute precision although the sequence is possible: gamma / xi
+ *                        of that step are not representable (fp32 range; use fp64)     */
 
 int32_t loghmm_abi_version(void);
 size_t loghmm_model_bytes(void); /* sizeof(loghmm_model_t), for binding checks */

@@ -991,6 +991,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) fb_post_kernel(co
     for (int v = 0; v < 2; ++v)
       for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][v][qq] = R(0);
   R* mw = wv + wid * 64;
+  bool range_bad = false;  // alpha~ . beta~ or alpha~^T A w underflowed (see the flag word, bit 2)
   __syncthreads();
   for (int c0 = t0; c0 < t1; c0 += TC) {
     for (int tt = wid; tt < TC; tt += kPostWarps) {
@@ -1013,6 +1014,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) fb_post_kernel(co
           qe[s] = act[s] ? qws[(int64_t)t * K + is[s]] : R(0);
         }
         const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
+        range_bad |= !(gz > R(0));
         const R yv0 = y0g[t], yv1 = two ? y1g[t] : R(0);
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
@@ -1055,6 +1057,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) fb_post_kernel(co
 #pragma unroll
       for (int s = 0; s < 2; ++s) qv[s] = row_dot64<R>(As + is[s] * PITCH, mw);
       const R Z = warp_sum(ap[0] * qv[0] + ap[1] * qv[1]);
+      range_bad |= !(Z > R(0));
       const R iz = R(1) / Z;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
@@ -1097,6 +1100,8 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) fb_post_kernel(co
     }
     __syncthreads();
   }
+  if (range_bad && lane == 0 && a.flags && isfinite(a.ll[b]))
+    atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 2 * b + 1), 4ull);
   // fold the statistics over the warps in order
   double* gts = sts + 2 * 64 * LOGHMM_NSLOT;  // [2][64]: gamma totals, first gamma
   for (int e = tid; e < 2 * 64 * LOGHMM_NSLOT + 2 * 64; e += blockDim.x) sts[e] = 0.0;
@@ -1201,6 +1206,7 @@ __global__ void __launch_bounds__(256, 2) fb_post_sparse_kernel(const FBArgs a, 
     for (int v = 0; v < 2; ++v)
 #pragma unroll
       for (int qq = 0; qq < LOGHMM_NSLOT; ++qq) st[s][v][qq] = R(0);
+  bool range_bad = false;  // alpha~ . beta~ or alpha~^T A w underflowed (flag word, bit 2)
   // this step's inputs are loaded one step ahead (the next step's loads are in
   // flight while the current one is reduced)
   R nat[2], nqe[2], nap[2], nwj[2], ny0 = R(0), ny1 = R(0);
@@ -1229,6 +1235,7 @@ __global__ void __launch_bounds__(256, 2) fb_post_sparse_kernel(const FBArgs a, 
     const R yv0 = ny0, yv1 = ny1;
     fetch(t + kPostWarps);
     const R gz = warp_sum(at[0] * qe[0] + at[1] * qe[1]);
+    range_bad |= !(gz > R(0));
     const R igz = R(1) / gz;  // one division per step (posteriors stay within 1 ulp of a per-state division)
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -1259,6 +1266,7 @@ __global__ void __launch_bounds__(256, 2) fb_post_sparse_kernel(const FBArgs a, 
       qv[s] = acc;
     }
     const R Z = warp_sum(ap[0] * qv[0] + ap[1] * qv[1]);
+    range_bad |= !(Z > R(0));
     const R iz = R(1) / Z;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -1267,6 +1275,8 @@ __global__ void __launch_bounds__(256, 2) fb_post_sparse_kernel(const FBArgs a, 
       for (int n = 0; n < NZ; ++n) xs[s][n] = fma(ta, mw[tgt[s][n]], xs[s][n]);
     }
   }
+  if (range_bad && lane == 0 && a.flags && isfinite(a.ll[b]))
+    atomicOr(reinterpret_cast<unsigned long long*>(a.flags + 2 * b + 1), 4ull);
   // fold the statistics and the xi sums over the warps in order
   double* gts = sts + 2 * 64 * LOGHMM_NSLOT;  // [2][64]: gamma totals, first gamma
   for (int e = tid; e < 2 * 64 * LOGHMM_NSLOT + 2 * 64 + 64 * NZ; e += blockDim.x) sts[e] = 0.0;

@@ -154,6 +154,10 @@ def validate_sequence(values) -> np.ndarray:
     return seq
 
 
+RANGE_MSG = ("the forward and backward vectors of sequence {s} are further apart than the compute "
+             "precision's exponent range at some step (posteriors not representable): use dtype='float64'")
+
+
 def _raise_flags(flags: np.ndarray, ll: np.ndarray | None, infeasible_msg: str | None):
     if (flags[:, 1] & 1).any():
         raise ValueError("observation sequence contains NaN")
@@ -161,6 +165,11 @@ def _raise_flags(flags: np.ndarray, ll: np.ndarray | None, infeasible_msg: str |
         bad = np.nonzero(ll == -np.inf)[0]
         if bad.size:
             raise InfeasibleSequenceError(infeasible_msg)
+    # (no reference counterpart: the reference computes in fp64 log space; the
+    # large-K fp32 path reports the loss of range instead of returning NaN)
+    rng = np.nonzero(flags[:, 1] & 4)[0]
+    if rng.size:
+        raise FloatingPointError(RANGE_MSG.format(s=int(rng[0])))
 
 
 def _single(model: HmmModel, sequence, dtype):

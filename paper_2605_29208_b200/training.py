@@ -225,6 +225,11 @@ def _check_estep(flags: np.ndarray, ll: np.ndarray) -> None:
                 f"sequence {s}, index {int(flags[s, 0])}"
             )
         raise TrainingError(f"sequence {s} is impossible under the model")
+    rng = np.nonzero(flags[:, 1] & 4)[0]
+    if rng.size:
+        from .inference import RANGE_MSG
+
+        raise FloatingPointError(RANGE_MSG.format(s=int(rng[0])))
 
 
 def baum_welch(model: HmmModel, data, config: TrainingConfig | None = None, dtype="float64"):

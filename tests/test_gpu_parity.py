@@ -779,6 +779,22 @@ def _check_banded_fb(K, half, dtype, variant, sparse, monkeypatch):
     np.testing.assert_allclose(fitted.transitions, A2, atol=1e-9 if f64 else 1e-4)
 
 
+def test_large_k_fp32_range_is_reported_not_nan():
+    """K > 8 in fp32: a start that is wildly inconsistent with the data puts
+    the max-normalised forward and backward vectors further apart than fp32's
+    exponent range.  The reference (fp64 log space) and the fp64 path return
+    finite posteriors; the fp32 path must say so instead of returning NaN."""
+    rng = np.random.default_rng(1764)
+    m = _banded_model(rng, 64, 4, dead_first=True)  # all initial mass on the rate-32 state
+    seqs = [rng.poisson(6.0, n).astype(float) for n in (17, 700)]
+    r64 = H.posteriors_batch(m, seqs, dtype="float64")
+    assert torch.isfinite(r64.gamma).all()
+    with pytest.raises(FloatingPointError, match="float64"):
+        H.posteriors_batch(m, seqs, dtype="float32")
+    with pytest.raises(FloatingPointError, match="float64"):
+        H.baum_welch(m, seqs, H.TrainingConfig(max_iterations=2), dtype="float32")
+
+
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_error_semantics_equal_length_batches(dtype):
     """Error paths of the equal-length decomposition (chunk operators + meet in
