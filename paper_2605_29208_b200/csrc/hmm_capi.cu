@@ -465,16 +465,28 @@ int32_t loghmm_forward_backward(int32_t dtype, const loghmm_model_t* h_desc,
     else if (lps == 2) fb_large_kernel<RR, KMV, 2><<<(unsigned)B, threads, smem, st>>>(a, K, (const RR*)lbw); \
     else fb_large_kernel<RR, KMV, 1><<<(unsigned)B, threads, smem, st>>>(a, K, (const RR*)lbw); \
   } while (0)
+    // (the per-sequence kernel of the large-K Viterbi: state parameters in
+    // registers, coalesced rows; no flag word here, the sweeps report NaN)
+    VitArgs ea{};
+    ea.model = model;
+    ea.y0 = y0;
+    ea.y1 = a.y1;
+    ea.offsets = offsets;
+    ea.B = B;
+    ea.lut = lgamma_lut;
+    ea.lut_n = lut_n;
+    ea.n_streams = a.n_streams;
+    ea.flags = nullptr;
+    const dim3 egrid((unsigned)((max_T + kEmSeqChunk - 1) / kEmSeqChunk), (unsigned)B);
+    (void)eblocks;
     if (dtype == LOGHMM_F64) {
-      emission_kernel<double><<<(unsigned)eblocks, 256, 0, st>>>(
-          model, (const double*)y0, (const double*)a.y1, N, K, lgamma_lut, lut_n, (double*)lbw);
+      emission_seq_kernel<double><<<egrid, 256, 0, st>>>(ea, K, (double*)lbw);
       if (split) e = launch_split<double>(a, K, KM, lps, B, threads, lbw, workspace, N, esz, partials != nullptr, st);
       else if (KM == 16) LHMM_FBL(double, 16);
       else if (KM == 32) LHMM_FBL(double, 32);
       else LHMM_FBL(double, 64);
     } else {
-      emission_kernel<float><<<(unsigned)eblocks, 256, 0, st>>>(
-          model, (const float*)y0, (const float*)a.y1, N, K, lgamma_lut, lut_n, (float*)lbw);
+      emission_seq_kernel<float><<<egrid, 256, 0, st>>>(ea, K, (float*)lbw);
       if (split) {
         e = launch_split<float>(a, K, KM, lps, B, threads, lbw, workspace, N, esz, partials != nullptr, st);
       } else if (KM == 16) LHMM_FBL(float, 16);
