@@ -118,6 +118,10 @@ class Pipeline:
 
     def load(self, y) -> None:
         """Copy observations [B, T] (or [B, T, 2]) into the device batch."""
+        if self.ns == 2 and isinstance(y, (tuple, list)):
+            self.y0.copy_(torch.as_tensor(y[0]).reshape(-1), non_blocking=True)
+            self.y1.copy_(torch.as_tensor(y[1]).reshape(-1), non_blocking=True)
+            return
         y = torch.as_tensor(y)
         if self.ns == 1:
             self.y0.copy_(y.reshape(-1), non_blocking=True)
@@ -260,8 +264,13 @@ class Pipeline:
         """One step whose observations come from (pinned) host memory, with
         the host-to-device copy of each slice overlapped with the kernels of
         the slices before it."""
-        y = torch.as_tensor(y_host)
-        ys = [y.reshape(-1)] if self.ns == 1 else [y[..., 0].reshape(-1), y[..., 1].reshape(-1)]
+        if self.ns == 2 and isinstance(y_host, (tuple, list)):
+            # two pinned 1-D streams (a [B, T, 2] array's per-stream views are
+            # strided: flattening them would stage through pageable memory)
+            ys = [torch.as_tensor(y_host[0]).reshape(-1), torch.as_tensor(y_host[1]).reshape(-1)]
+        else:
+            y = torch.as_tensor(y_host)
+            ys = [y.reshape(-1)] if self.ns == 1 else [y[..., 0].reshape(-1), y[..., 1].reshape(-1)]
         dst = [self.y0] if self.ns == 1 else [self.y0, self.y1]
         main = torch.cuda.current_stream(self.dev)
         plans = self._slice_plan(slices)
